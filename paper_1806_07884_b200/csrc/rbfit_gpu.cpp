@@ -1,0 +1,298 @@
+// rbfit_gpu.cpp -- reference-shaped C++ API over the C ABI (see rbfit_gpu.hpp).
+#include "rbfit_gpu.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <memory>
+
+#include "rbg.h"
+
+namespace rbfit_b200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+[[noreturn]] void raise(rbg_status st, const std::string& msg) {
+    switch (st) {
+        case RBG_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case RBG_DOMAIN_ERROR: throw std::domain_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+void check(rbg_status st, rbg_ctx* ctx) {
+    if (st != RBG_OK) raise(st, rbg_last_error(ctx));
+}
+
+int family_id(KernelFamily f) { return static_cast<int>(f); }
+
+struct NameEntry {
+    KernelFamily family;
+    std::string_view name;
+};
+constexpr NameEntry kNames[] = {  // kernel.cpp:13-18 + the wendland-3-2 extension
+    {KernelFamily::wendland_3_0, "wendland-3-0"},
+    {KernelFamily::wendland_3_1, "wendland-3-1"},
+    {KernelFamily::wendland_3_3, "wendland-3-3"},
+    {KernelFamily::wendland_3_2, "wendland-3-2"},
+};
+
+const double* flat(std::span<const Point2> p) { return reinterpret_cast<const double*>(p.data()); }
+
+// Device context: the caller's or a temporary one.
+struct Using {
+    std::unique_ptr<Device> own;
+    Device* dev;
+    explicit Using(Device* d, int index = 0) : dev(d) {
+        if (!dev) {
+            own = std::make_unique<Device>(index);
+            dev = own.get();
+        }
+    }
+    rbg_ctx* ctx() const { return dev->ctx(); }
+};
+
+void set_centres(rbg_ctx* ctx, std::span<const Point2> refs, const KernelSpec& kernel) {
+    check(rbg_set_centres(ctx, 2, flat(refs), refs.size(), family_id(kernel.family()),
+                          kernel.alpha()),
+          ctx);
+}
+
+}  // namespace
+
+KernelFamily kernel_from_name(std::string_view name) {
+    for (const auto& e : kNames)
+        if (e.name == name) return e.family;
+    std::string msg = "unknown kernel '" + std::string(name) + "'; expected one of:";
+    for (const auto& e : kNames) msg += " " + std::string(e.name);
+    throw std::invalid_argument(msg);
+}
+
+std::string_view kernel_name(KernelFamily family) {
+    for (const auto& e : kNames)
+        if (e.family == family) return e.name;
+    throw std::invalid_argument("unknown kernel family");
+}
+
+KernelSpec::KernelSpec(KernelFamily family, double alpha) : family_(family), alpha_(alpha) {
+    if (!(alpha > 0.0) || !std::isfinite(alpha))
+        throw std::invalid_argument("kernel shape parameter must be positive and finite");
+}
+
+double KernelSpec::evaluate(double r) const {
+    double out = 0.0;
+    const rbg_status st = rbg_kernel_value(family_id(family_), alpha_, r, &out);
+    if (st == RBG_DOMAIN_ERROR)
+        throw std::domain_error("kernel evaluate: radius must be finite and non-negative");
+    if (st != RBG_OK) throw std::invalid_argument("kernel evaluate: bad kernel");
+    return out;
+}
+
+Device::Device(int device) {
+    const rbg_status st = rbg_create(device, &ctx_);
+    if (st != RBG_OK)
+        raise(st, "cannot create a GPU context on device " + std::to_string(device));
+}
+
+Device::~Device() {
+    if (ctx_) rbg_destroy(ctx_);
+}
+
+void Device::set_stream(void* s) { check(rbg_set_stream(ctx_, s), ctx_); }
+
+double NormalSystem::at(std::size_t i, std::size_t j) const {
+    if (i > j) std::swap(i, j);
+    const auto b = cols.begin() + static_cast<std::ptrdiff_t>(row_ptr[i]);
+    const auto e = cols.begin() + static_cast<std::ptrdiff_t>(row_ptr[i + 1]);
+    const auto it = std::lower_bound(b, e, static_cast<std::uint32_t>(j));
+    return (it != e && *it == j) ? values[static_cast<std::size_t>(it - cols.begin())] : 0.0;
+}
+
+NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
+                                 const KernelSpec& kernel, bool poly, BuildStats* stats,
+                                 Device* device, const AllReduce& allreduce) {
+    if (cloud.values.size() != cloud.points.size())  // solver.cpp:135-136
+        throw std::invalid_argument("build_normal_system: value count does not match points");
+    if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
+    if (poly)
+        throw std::invalid_argument(
+            "build_normal_system: the linear-polynomial border is not implemented on the GPU path");
+    Using u(device);
+    rbg_ctx* ctx = u.ctx();
+    BuildStats local{};
+    auto t0 = Clock::now();
+    set_centres(ctx, refs, kernel);
+    local.index_seconds = seconds_since(t0);
+    t0 = Clock::now();
+    check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
+    if (allreduce) {
+        double* buf = nullptr;
+        std::uint64_t count = 0;
+        check(rbg_system_device(ctx, &buf, &count), ctx);
+        allreduce(buf, count, nullptr);
+    }
+    rbg_pattern_info info{};
+    check(rbg_get_pattern_info(ctx, &info), ctx);
+    const std::size_t m = refs.size();
+    NormalSystem sys;
+    sys.side = m;
+    sys.row_ptr.resize(m + 1);
+    sys.cols.resize(info.nnz_upper);
+    sys.values.resize(info.nnz_upper);
+    sys.rhs.resize(m);
+    std::vector<double> hits(m);
+    std::uint64_t design_nnz = 0;
+    check(rbg_get_system(ctx, sys.values.data(), sys.rhs.data(), hits.data(), &design_nnz), ctx);
+    local.assembly_seconds = seconds_since(t0);
+    check(rbg_get_pattern(ctx, sys.row_ptr.data(), sys.cols.data()), ctx);
+    for (std::size_t j = 0; j < m; ++j)
+        if (hits[j] == 0.0) sys.empty_support_refs.push_back(static_cast<std::uint32_t>(j));
+    local.design_nnz = design_nnz;
+    local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);
+    if (stats) *stats = local;
+    return sys;
+}
+
+Weights solve_weights(const NormalSystem& sys, SolveDiag* diag, Device* device) {
+    if (sys.side == 0 || sys.rhs.size() != sys.side || sys.row_ptr.size() != sys.side + 1 ||
+        sys.values.size() != sys.cols.size())
+        throw std::invalid_argument("solve_weights: malformed normal system");
+    if (!device)
+        throw std::invalid_argument(
+            "solve_weights: pass the Device that assembled the system (the pattern lives there)");
+    rbg_ctx* ctx = device->ctx();
+    rbg_pattern_info info{};
+    check(rbg_get_pattern_info(ctx, &info), ctx);
+    if (info.m != sys.side || info.nnz_upper != sys.values.size())
+        throw std::invalid_argument("solve_weights: system does not match the device's pattern");
+    check(rbg_set_system(ctx, sys.values.data(), sys.rhs.data(), nullptr), ctx);
+    Weights w;
+    w.c.resize(sys.side);
+    rbg_solve_diag d{};
+    check(rbg_solve(ctx, nullptr, w.c.data(), &d), ctx);
+    if (diag) *diag = SolveDiag{d.ridge_lambda, d.ridge_shift, d.attempts, d.iterations, d.rel_residual};
+    return w;
+}
+
+Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& kernel,
+          const FitOptions& options, FitReport* report) {
+    if (cloud.size() == 0) throw std::invalid_argument("fit: empty point cloud");  // solver.cpp:403-406
+    if (cloud.values.size() != cloud.points.size())
+        throw std::invalid_argument("fit: cloud value count mismatch");
+    if (refs.empty()) throw std::invalid_argument("fit: no reference points");
+    if (options.poly)
+        throw std::invalid_argument("fit: the linear-polynomial border is not implemented on the GPU path");
+
+    FitReport local{};
+    if (cloud.size() < refs.size())
+        local.warnings.push_back(
+            "fewer data points than reference points; the least-squares system is "
+            "underdetermined");
+    const std::size_t m = refs.size();
+    local.plan = BlockPlan{m, m, 1, options.ram_budget_bytes, options.prec_bytes, true};
+
+    Device dev(options.device);
+    rbg_ctx* ctx = dev.ctx();
+    auto t0 = Clock::now();
+    set_centres(ctx, refs, kernel);
+    local.index_seconds = seconds_since(t0);
+    t0 = Clock::now();
+    check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
+    if (options.allreduce) {
+        double* buf = nullptr;
+        std::uint64_t count = 0;
+        check(rbg_system_device(ctx, &buf, &count), ctx);
+        options.allreduce(buf, count, nullptr);
+    }
+    std::vector<double> hits(m);
+    std::uint64_t design_nnz = 0;
+    check(rbg_get_system(ctx, nullptr, nullptr, hits.data(), &design_nnz), ctx);
+    local.assembly_seconds = seconds_since(t0);
+    t0 = Clock::now();
+    std::vector<double> c(m);
+    rbg_solve_options so{options.tol, options.max_iter};
+    rbg_solve_diag d{};
+    check(rbg_solve(ctx, &so, c.data(), &d), ctx);
+    local.gram_solve_seconds = seconds_since(t0);
+    local.design_nnz = design_nnz;
+    for (std::size_t j = 0; j < m; ++j)
+        if (hits[j] == 0.0) local.empty_support_refs.push_back(static_cast<std::uint32_t>(j));
+    local.ridge_lambda = d.ridge_lambda;
+    local.ridge_shift = d.ridge_shift;
+    local.iterations = d.iterations;
+    if (d.ridge_lambda > 0.0)
+        local.warnings.push_back(
+            "normal equations numerically singular; ridge solution kept (the orthogonal "
+            "re-pass is not implemented on the GPU path)");
+    rbg_pattern_info info{};
+    check(rbg_get_pattern_info(ctx, &info), ctx);
+    local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);
+
+    Model model{kernel, std::move(refs), std::move(c), std::nullopt, cloud.offset};
+    if (report) *report = std::move(local);
+    return model;
+}
+
+std::vector<double> evaluate_model(const Model& model, std::span<const Point2> queries,
+                                   Device* device) {
+    if (model.refs.empty()) throw std::invalid_argument("model has no reference points");
+    if (model.weights.size() != model.refs.size())
+        throw std::invalid_argument("model weight count does not match reference count");
+    if (model.poly)
+        throw std::invalid_argument("evaluate_model: polynomial models are not supported on the GPU path");
+    Using u(device);
+    set_centres(u.ctx(), model.refs, model.kernel);
+    std::vector<Point2> shifted;
+    std::span<const Point2> q = queries;
+    if (model.offset.x != 0.0 || model.offset.y != 0.0) {  // model.cpp:192-194
+        shifted.resize(queries.size());
+        for (std::size_t i = 0; i < queries.size(); ++i)
+            shifted[i] = {queries[i].x + -model.offset.x, queries[i].y + -model.offset.y};
+        q = shifted;
+    }
+    std::vector<double> f(q.size());
+    check(rbg_evaluate(u.ctx(), model.weights.data(), flat(q), q.size(), f.data()), u.ctx());
+    return f;
+}
+
+ErrorReport error_report(const Model& model, const PointCloud& cloud,
+                         std::optional<std::size_t> design_nnz, Device* device) {
+    if (cloud.size() == 0) throw std::invalid_argument("error_report: empty cloud");
+    if (cloud.values.size() != cloud.points.size())
+        throw std::invalid_argument("error_report: cloud value count mismatch");
+    if (model.weights.size() != model.refs.size())
+        throw std::invalid_argument("model weight count does not match reference count");
+    Using u(device);
+    set_centres(u.ctx(), model.refs, model.kernel);
+    const Point2 delta{cloud.offset.x - model.offset.x, cloud.offset.y - model.offset.y};
+    std::vector<Point2> shifted;
+    std::span<const Point2> q = cloud.points;
+    if (delta.x != 0.0 || delta.y != 0.0) {  // model.cpp:202-204
+        shifted.resize(cloud.size());
+        for (std::size_t i = 0; i < cloud.size(); ++i)
+            shifted[i] = {cloud.points[i].x + delta.x, cloud.points[i].y + delta.y};
+        q = shifted;
+    }
+    ErrorReport rep;
+    rep.signed_errors.resize(cloud.size());
+    rbg_error_stats st{};
+    check(rbg_error_report(u.ctx(), model.weights.data(), flat(q), cloud.values.data(), cloud.size(),
+                           &st, rep.signed_errors.data()),
+          u.ctx());
+    rep.mean_absolute_error = st.mean_absolute_error;
+    rep.deviation_of_error = st.deviation_of_error;
+    rep.mean_relative_error_pct = st.mean_relative_error_pct;
+    rep.rms_error = st.rms_error;
+    rep.max_abs_error = st.max_abs_error;
+    if (design_nnz)
+        rep.density_pct = 100.0 * static_cast<double>(*design_nnz) /
+                          (static_cast<double>(cloud.size()) * static_cast<double>(model.refs.size()));
+    return rep;
+}
+
+}  // namespace rbfit_b200

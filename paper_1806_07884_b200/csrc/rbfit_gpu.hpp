@@ -1,0 +1,179 @@
+// rbfit_gpu.hpp -- C++ host layer with the reference's hot-path API
+// (rbfit::fit / build_normal_system / solve_weights / evaluate_model /
+// error_report, /root/reference/proj/core/include/rbfit/{solver,model}.hpp),
+// executing on the B200 through the C ABI in include/rbg.h.
+//
+// Drop-in notes:
+//  * same names, argument meaning and exception classes (std::invalid_argument,
+//    std::runtime_error, std::domain_error) and the same messages where the
+//    reference states them;
+//  * NormalSystem is sparse (upper CSR) instead of dense side x side: at the
+//    BASELINE sizes the dense matrix does not exist in any memory;
+//  * the block planner (BlockPlan / ram budget) has no GPU meaning: the whole
+//    pattern is resident; FitReport::plan reports one block;
+//  * the linear-polynomial border (--poly) and the orthogonal re-pass are not
+//    implemented on the GPU path (std::invalid_argument / warning).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+struct rbg_ctx;
+
+namespace rbfit_b200 {
+
+struct Point2 {  // layout-identical to rbfit::Point2 (geometry.hpp:9-12)
+    double x = 0.0;
+    double y = 0.0;
+};
+
+struct PointCloud {  // rbfit::PointCloud (data.hpp:17-23)
+    std::vector<Point2> points;
+    std::vector<double> values;
+    Point2 offset{0.0, 0.0};
+    std::size_t size() const { return points.size(); }
+};
+
+enum class KernelFamily { wendland_3_0, wendland_3_1, wendland_3_3, wendland_3_2 };
+KernelFamily kernel_from_name(std::string_view name);
+std::string_view kernel_name(KernelFamily family);
+
+class KernelSpec {  // rbfit::KernelSpec (kernel.hpp:32-71)
+  public:
+    KernelSpec(KernelFamily family, double alpha);
+    KernelFamily family() const { return family_; }
+    double alpha() const { return alpha_; }
+    double support_radius() const { return 1.0 / alpha_; }
+    double evaluate(double r) const;  // bitwise the device's phi
+    double operator()(double r) const { return evaluate(r); }
+
+  private:
+    KernelFamily family_;
+    double alpha_;
+};
+
+// One GPU engine context (owns an rbg_ctx).  Not thread-safe.
+class Device {
+  public:
+    explicit Device(int device = 0);
+    ~Device();
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+    rbg_ctx* ctx() const { return ctx_; }
+    void set_stream(void* cuda_stream);
+
+  private:
+    rbg_ctx* ctx_ = nullptr;
+};
+
+// NormalSystem (solver.hpp:61-69) in upper-CSR form.
+struct NormalSystem {
+    std::size_t side = 0;
+    std::vector<std::uint64_t> row_ptr;  // side + 1
+    std::vector<std::uint32_t> cols;     // ascending per row, cols >= row
+    std::vector<double> values;
+    std::vector<double> rhs;
+    bool poly = false;
+    std::vector<std::uint32_t> empty_support_refs;
+    double at(std::size_t i, std::size_t j) const;  // symmetric lookup, 0 off-pattern
+};
+
+struct BuildStats {  // solver.hpp:71-78 (device times)
+    double index_seconds = 0.0;     // centre binning + symbolic pattern
+    double assembly_seconds = 0.0;  // point binning + numeric assembly (incl. copies)
+    double gram_seconds = 0.0;      // fused into assembly on the GPU (0)
+    std::size_t peak_bytes = 0;
+    std::size_t design_nnz = 0;
+    std::size_t blocks_assembled = 1;
+};
+
+// Sum-allreduce hook for multi-GPU builds: called with the device buffer
+// [values | rhs | hits] (fp64) after the local slab is assembled, on the
+// context's stream (e.g. wraps ncclAllReduce(..., ncclFloat64, ncclSum)).
+using AllReduce = std::function<void(double* device_buffer, std::uint64_t count, void* stream)>;
+
+NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
+                                 const KernelSpec& kernel, bool poly, BuildStats* stats = nullptr,
+                                 Device* device = nullptr, const AllReduce& allreduce = {});
+
+struct SolveDiag {  // solver.hpp:96-100
+    double ridge_lambda = 0.0;
+    double ridge_shift = 0.0;
+    int attempts = 0;
+    int iterations = 0;
+    double rel_residual = 0.0;
+};
+
+struct Weights {  // solver.hpp:102-105
+    std::vector<double> c;
+    std::optional<std::array<double, 3>> poly;
+};
+
+Weights solve_weights(const NormalSystem& sys, SolveDiag* diag = nullptr, Device* device = nullptr);
+
+struct FitOptions {  // solver.hpp:113-118 (+ GPU solve controls)
+    bool poly = false;
+    std::size_t ram_budget_bytes = std::size_t{1} << 30;  // accepted, unused on the GPU
+    std::size_t prec_bytes = 8;
+    std::optional<std::size_t> block_size;  // accepted, unused on the GPU
+    double tol = 1e-12;
+    int max_iter = 20000;
+    int device = 0;
+    AllReduce allreduce;  // multi-GPU: sum partial systems across ranks
+};
+
+struct BlockPlan {
+    std::size_t m_total = 0, block_size = 0, n_blocks = 1, ram_budget_bytes = 0, prec_bytes = 8;
+    bool sparse_mode = true;
+};
+
+struct FitReport {  // solver.hpp:120-131
+    BlockPlan plan;
+    double index_seconds = 0.0;
+    double assembly_seconds = 0.0;
+    double gram_solve_seconds = 0.0;
+    std::size_t peak_bytes = 0;
+    std::size_t design_nnz = 0;
+    std::vector<std::uint32_t> empty_support_refs;
+    double ridge_lambda = 0.0;
+    double ridge_shift = 0.0;
+    int iterations = 0;
+    std::vector<std::string> warnings;
+};
+
+struct Model {  // model.hpp:17-23
+    KernelSpec kernel;
+    std::vector<Point2> refs;
+    std::vector<double> weights;
+    std::optional<std::array<double, 3>> poly;
+    Point2 offset{0.0, 0.0};
+};
+
+Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& kernel,
+          const FitOptions& options = {}, FitReport* report = nullptr);
+
+std::vector<double> evaluate_model(const Model& model, std::span<const Point2> queries,
+                                   Device* device = nullptr);
+
+struct ErrorReport {  // model.hpp:38-50 (+ rms, max)
+    double mean_absolute_error = 0.0;
+    double deviation_of_error = 0.0;
+    double mean_relative_error_pct = 0.0;
+    double rms_error = 0.0;
+    double max_abs_error = 0.0;
+    std::vector<double> signed_errors;
+    std::optional<double> density_pct;
+};
+
+ErrorReport error_report(const Model& model, const PointCloud& cloud,
+                         std::optional<std::size_t> design_nnz = std::nullopt,
+                         Device* device = nullptr);
+
+}  // namespace rbfit_b200

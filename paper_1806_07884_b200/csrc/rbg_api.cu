@@ -1,0 +1,403 @@
+// rbg_api.cu -- the C ABI (include/rbg.h): validation with the reference's
+// messages, host<->device staging, status codes.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#include "rbg_internal.cuh"
+
+using rbg::Error;
+
+namespace {
+
+template <typename F>
+rbg_status guarded(rbg_ctx* ctx, F&& f) {
+    if (!ctx) return RBG_INVALID_ARGUMENT;
+    try {
+        ctx->err.clear();
+        f();
+        return RBG_OK;
+    } catch (const Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "host allocation failed";
+        return RBG_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return RBG_RUNTIME_ERROR;
+    }
+}
+
+void bind(rbg_ctx* ctx) { RBG_CUDA(cudaSetDevice(ctx->device)); }
+
+void require_centres(const rbg_ctx* ctx) {
+    if (!ctx->have_centres)
+        throw Error(RBG_NOT_READY, "no reference points set (call rbg_set_centres first)");
+}
+void require_system(const rbg_ctx* ctx) {
+    require_centres(ctx);
+    if (!ctx->have_system)
+        throw Error(RBG_NOT_READY, "no assembled system (call rbg_assemble first)");
+}
+
+void check_points_finite(const double* p, uint64_t n, int dim, const char* what) {
+    for (uint64_t i = 0; i < n; ++i)
+        for (int d = 0; d < dim; ++d)
+            if (!std::isfinite(p[i * dim + d]))
+                throw Error(RBG_INVALID_ARGUMENT,
+                            std::string(what) + std::to_string(i));
+}
+
+void check_misses(rbg_ctx* ctx) {
+    unsigned long long miss = 0;
+    RBG_CUDA(cudaMemcpyAsync(&miss, ctx->counters.p, sizeof(miss), cudaMemcpyDeviceToHost, ctx->stream));
+    RBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (miss)
+        throw Error(RBG_RUNTIME_ERROR, "internal: " + std::to_string(miss) +
+                                           " assembly updates fell outside the symbolic pattern");
+}
+
+// Host copy of the device kernel (kernel.hpp:42-62); x86-64 baseline has no
+// FMA, so this is the reference's arithmetic.
+double phi_host(int family, double alpha, double r) {
+    const double t = alpha * r;
+    if (!(t < 1.0)) return 0.0;
+    const double u = 1.0 - t;
+    switch (family) {
+        case RBG_WENDLAND_3_0: return u * u;
+        case RBG_WENDLAND_3_1: {
+            const double u2 = u * u;
+            return u2 * u2 * (4.0 * t + 1.0);
+        }
+        case RBG_WENDLAND_3_3: {
+            const double u2 = u * u, u4 = u2 * u2;
+            return u4 * u4 * (((32.0 * t + 25.0) * t + 8.0) * t + 1.0);
+        }
+        default: {
+            const double u2 = u * u, u4 = u2 * u2, u6 = u4 * u2;
+            return u6 * ((35.0 * t + 18.0) * t + 3.0);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+rbg_status rbg_create(int device, rbg_ctx** out) {
+    if (!out) return RBG_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* ctx = new rbg_ctx();
+    ctx->device = device;
+    const rbg_status s = guarded(ctx, [&] {
+        int n = 0;
+        RBG_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n)
+            throw Error(RBG_INVALID_ARGUMENT, "CUDA device " + std::to_string(device) +
+                                                  " does not exist (" + std::to_string(n) + " visible)");
+        bind(ctx);
+        RBG_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+        RBG_CUDA(cudaEventCreate(&ctx->ev0));
+        RBG_CUDA(cudaEventCreate(&ctx->ev1));
+        for (auto& e : ctx->ev_asm) RBG_CUDA(cudaEventCreate(&e));
+    });
+    if (s != RBG_OK) {
+        // keep the message reachable through a static buffer
+        static thread_local std::string last;
+        last = ctx->err;
+        delete ctx;
+        return s;
+    }
+    *out = ctx;
+    return RBG_OK;
+}
+
+rbg_status rbg_destroy(rbg_ctx* ctx) {
+    if (!ctx) return RBG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (auto& e : ctx->ev_asm)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+    return RBG_OK;
+}
+
+const char* rbg_last_error(const rbg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+rbg_status rbg_set_stream(rbg_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] { ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream; });
+}
+
+rbg_status rbg_synchronize(rbg_ctx* ctx) {
+    return guarded(ctx, [&] {
+        bind(ctx);
+        RBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uint64_t rbg_launch_count(const rbg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_t m, int family,
+                           double alpha) {
+    return guarded(ctx, [&] {
+        if (dim != 2 && dim != 3) throw Error(RBG_INVALID_ARGUMENT, "dimension must be 2 or 3");
+        if (family < 0 || family > 3) throw Error(RBG_INVALID_ARGUMENT, "unknown kernel family");
+        if (!(alpha > 0.0) || !std::isfinite(alpha))  // kernel.cpp:35-38
+            throw Error(RBG_INVALID_ARGUMENT, "kernel shape parameter must be positive and finite");
+        if (m == 0 || !centres)  // coo.cpp:168
+            throw Error(RBG_INVALID_ARGUMENT, "assemble_submatrix: empty reference block");
+        if (m > 0xffffffffull)  // coo.cpp:13-16
+            throw Error(RBG_INVALID_ARGUMENT, "reference count exceeds 32-bit triplet index range");
+        check_points_finite(centres, m, dim, "non-finite reference point at index ");  // coo.cpp:172-175
+        bind(ctx);
+        ctx->have_centres = false;
+        ctx->have_system = false;
+        ctx->dim = dim;
+        ctx->m = m;
+        ctx->family = family;
+        ctx->alpha = alpha;
+        ctx->radius = 1.0 / alpha;                // kernel.hpp:37
+        ctx->r2 = ctx->radius * ctx->radius;      // kdtree.cpp:64
+        ctx->centres.reserve(m * dim);
+        RBG_CUDA(cudaMemcpyAsync(ctx->centres.p, centres, m * dim * sizeof(double),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+        rbg::setup_centres(ctx);
+        RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        RBG_CUDA(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->setup_ms = ms;
+        ctx->have_centres = true;
+    });
+}
+
+rbg_status rbg_get_pattern_info(rbg_ctx* ctx, rbg_pattern_info* info) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (!info) throw Error(RBG_INVALID_ARGUMENT, "null info");
+        info->m = ctx->m;
+        info->nnz_upper = ctx->nnz_upper;
+        info->nnz_full = ctx->nnz_full;
+        info->n_tiles = ctx->grid.count;
+        info->n_fallback = ctx->n_fallback;
+        info->max_tile_centres = ctx->max_tile_centres;
+        info->tile_edge = ctx->grid.edge;
+        info->setup_ms = ctx->setup_ms;
+    });
+}
+
+rbg_status rbg_get_pattern(rbg_ctx* ctx, uint64_t* row_ptr, uint32_t* cols) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        bind(ctx);
+        if (row_ptr)
+            RBG_CUDA(cudaMemcpyAsync(row_ptr, ctx->uptr.p, (ctx->m + 1) * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        if (cols)
+            RBG_CUDA(cudaMemcpyAsync(cols, ctx->ucols.p, ctx->nnz_upper * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        RBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uint64_t n,
+                        int accumulate, int validate) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
+        if (validate) check_points_finite(points, n, ctx->dim, "non-finite coordinate at point index ");
+        bind(ctx);
+        if (n > 0) {
+            ctx->in_pts.reserve(n * ctx->dim);
+            ctx->in_h.reserve(n);
+            RBG_CUDA(cudaMemcpyAsync(ctx->in_pts.p, points, n * ctx->dim * sizeof(double),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+            RBG_CUDA(cudaMemcpyAsync(ctx->in_h.p, h, n * sizeof(double), cudaMemcpyHostToDevice,
+                                     ctx->stream));
+        }
+        rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
+    });
+}
+
+rbg_status rbg_assemble_device(rbg_ctx* ctx, const double* d_points, const double* d_h, uint64_t n,
+                               int accumulate) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        bind(ctx);
+        rbg::assemble_points(ctx, d_points, d_h, n, accumulate != 0);
+    });
+}
+
+rbg_status rbg_system_device(rbg_ctx* ctx, double** d_buffer, uint64_t* count) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (d_buffer) *d_buffer = ctx->sys.p;
+        if (count) *count = ctx->nnz_upper + 2 * ctx->m;
+    });
+}
+
+rbg_status rbg_get_system(rbg_ctx* ctx, double* values, double* rhs, double* hits,
+                          uint64_t* design_nnz) {
+    return guarded(ctx, [&] {
+        require_system(ctx);
+        bind(ctx);
+        check_misses(ctx);
+        cudaStream_t st = ctx->stream;
+        const uint64_t m = ctx->m;
+        if (values)
+            RBG_CUDA(cudaMemcpyAsync(values, ctx->sys.p, ctx->nnz_upper * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+        if (rhs)
+            RBG_CUDA(cudaMemcpyAsync(rhs, ctx->sys.p + ctx->nnz_upper, m * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+        std::vector<double> hbuf;
+        double* hp = hits;
+        if (!hp && design_nnz) {
+            hbuf.resize(m);
+            hp = hbuf.data();
+        }
+        if (hp)
+            RBG_CUDA(cudaMemcpyAsync(hp, ctx->sys.p + ctx->nnz_upper + m, m * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        if (design_nnz) {
+            uint64_t s = 0;
+            for (uint64_t i = 0; i < m; ++i) s += (uint64_t)hp[i];
+            *design_nnz = s;
+        }
+    });
+}
+
+rbg_status rbg_set_system(rbg_ctx* ctx, const double* values, const double* rhs, const double* hits) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (!values || !rhs) throw Error(RBG_INVALID_ARGUMENT, "null system array");
+        bind(ctx);
+        cudaStream_t st = ctx->stream;
+        RBG_CUDA(cudaMemcpyAsync(ctx->sys.p, values, ctx->nnz_upper * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(ctx->sys.p + ctx->nnz_upper, rhs, ctx->m * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+        if (hits)
+            RBG_CUDA(cudaMemcpyAsync(ctx->sys.p + ctx->nnz_upper + ctx->m, hits,
+                                     ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        ctx->have_system = true;
+    });
+}
+
+rbg_status rbg_solve(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rbg_solve_diag* diag) {
+    return guarded(ctx, [&] {
+        require_system(ctx);
+        bind(ctx);
+        check_misses(ctx);
+        rbg::solve_system(ctx, opts, c_out, diag);
+    });
+}
+
+rbg_status rbg_evaluate_device(rbg_ctx* ctx, const double* d_c, const double* d_q, uint64_t nq,
+                               double* d_f) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        bind(ctx);
+        rbg::evaluate_points(ctx, d_c, d_q, nq, d_f);
+    });
+}
+
+rbg_status rbg_evaluate(rbg_ctx* ctx, const double* c, const double* q, uint64_t nq, double* f) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (!c || (nq > 0 && (!q || !f))) throw Error(RBG_INVALID_ARGUMENT, "null array");
+        check_points_finite(q, nq, ctx->dim, "evaluate_model: non-finite query point at index ");
+        bind(ctx);
+        cudaStream_t st = ctx->stream;
+        ctx->ev_c.reserve(ctx->m);
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_c.p, c, ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (nq == 0) return;
+        ctx->ev_q.reserve(nq * ctx->dim);
+        ctx->ev_f.reserve(nq);
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_q.p, q, nq * ctx->dim * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+        rbg::evaluate_points(ctx, ctx->ev_c.p, ctx->ev_q.p, nq, ctx->ev_f.p);
+        RBG_CUDA(cudaMemcpyAsync(f, ctx->ev_f.p, nq * sizeof(double), cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points, const double* h,
+                            uint64_t n, rbg_error_stats* out, double* signed_errors) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (n == 0) throw Error(RBG_INVALID_ARGUMENT, "error_report: empty cloud");  // model.cpp:198
+        if (!c || !points || !h || !out) throw Error(RBG_INVALID_ARGUMENT, "null array");
+        bind(ctx);
+        cudaStream_t st = ctx->stream;
+        ctx->ev_c.reserve(ctx->m);
+        ctx->ev_q.reserve(n * ctx->dim);
+        ctx->ev_f.reserve(n);
+        ctx->ev_h.reserve(n);
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_c.p, c, ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_q.p, points, n * ctx->dim * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_h.p, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        rbg::evaluate_points(ctx, ctx->ev_c.p, ctx->ev_q.p, n, ctx->ev_f.p);
+        rbg::error_stats(ctx, ctx->ev_f.p, ctx->ev_h.p, n, out);
+        if (signed_errors) {
+            RBG_CUDA(cudaMemcpyAsync(signed_errors, ctx->ev_f.p, n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+            RBG_CUDA(cudaStreamSynchronize(st));
+            for (uint64_t i = 0; i < n; ++i) signed_errors[i] = signed_errors[i] - h[i];  // model.cpp:208
+        }
+    });
+}
+
+rbg_status rbg_partition_slabs(int dim, const double* points, uint64_t n, int axis, int n_slabs,
+                               double* bounds, uint32_t* slab_of) {
+    if ((dim != 2 && dim != 3) || axis < 0 || axis >= dim || n_slabs < 1 || !bounds ||
+        (n > 0 && !points))
+        return RBG_INVALID_ARGUMENT;
+    try {
+        std::vector<double> v(n);
+        for (uint64_t i = 0; i < n; ++i) v[i] = points[i * dim + axis];
+        bounds[0] = -std::numeric_limits<double>::infinity();
+        bounds[n_slabs] = std::numeric_limits<double>::infinity();
+        for (int k = 1; k < n_slabs; ++k) {
+            const uint64_t at = (uint64_t)((__int128)k * n / n_slabs);
+            if (at >= n) {
+                bounds[k] = std::numeric_limits<double>::infinity();
+                continue;
+            }
+            std::nth_element(v.begin(), v.begin() + at, v.end());
+            bounds[k] = v[at];
+        }
+        for (int k = 1; k < n_slabs; ++k)  // monotone (nth_element is per call)
+            if (bounds[k] < bounds[k - 1]) bounds[k] = bounds[k - 1];
+        if (slab_of)
+            for (uint64_t i = 0; i < n; ++i) {
+                const double x = points[i * dim + axis];
+                const int s = (int)(std::upper_bound(bounds + 1, bounds + n_slabs, x) - (bounds + 1));
+                slab_of[i] = (uint32_t)s;
+            }
+        return RBG_OK;
+    } catch (...) {
+        return RBG_RUNTIME_ERROR;
+    }
+}
+
+rbg_status rbg_kernel_value(int family, double alpha, double r, double* out) {
+    if (family < 0 || family > 3 || !(alpha > 0.0) || !std::isfinite(alpha) || !out)
+        return RBG_INVALID_ARGUMENT;
+    if (!(r >= 0.0) || !std::isfinite(r)) return RBG_DOMAIN_ERROR;  // kernel.hpp:43-44
+    *out = phi_host(family, alpha, r);
+    return RBG_OK;
+}
+
+}  // extern "C"

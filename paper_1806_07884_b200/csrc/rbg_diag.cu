@@ -1,0 +1,145 @@
+// rbg_diag.cu -- measurement helpers for the bench (not on the hot path):
+//  * support counts sum_p k_p and sum_p k_p^2 (the algorithmic work of an
+//    assembly), with the hot path's exact inclusion rule;
+//  * an fp64 FMA throughput microbenchmark (the fp64 roofline denominator,
+//    which MEASURED_PEAKS.json does not carry).
+#include <algorithm>
+
+#include "rbg_internal.cuh"
+
+namespace rbg {
+namespace {
+
+template <int DIM>
+__global__ void support_count_kernel(GridDev g, const uint64_t* __restrict__ cptr,
+                                     const uint32_t* __restrict__ cids,
+                                     const double* __restrict__ centres, int family, double alpha,
+                                     double r2, const double* __restrict__ q, uint64_t nq,
+                                     unsigned long long* out) {
+    unsigned long long s1 = 0, s2 = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = q[i * DIM], y = q[i * DIM + 1], z = DIM == 3 ? q[i * DIM + 2] : 0.0;
+        const uint64_t t = tile_of<DIM>(g, x, y, z);
+        unsigned long long k = 0;
+        if (t != ~0ull)
+            for (uint64_t e = cptr[t]; e < cptr[t + 1]; ++e) {
+                const uint32_t j = cids[e];
+                const double d2 = dist2_of<DIM>(x, y, z, centres[(uint64_t)j * DIM],
+                                                centres[(uint64_t)j * DIM + 1],
+                                                DIM == 3 ? centres[(uint64_t)j * DIM + 2] : 0.0);
+                if (d2 < r2 && phi_of_r(family, alpha, __dsqrt_rn(d2)) != 0.0) ++k;
+            }
+        s1 += k;
+        s2 += k * k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], s1);
+        atomicAdd(&out[1], s2);
+    }
+}
+
+constexpr int kChains = 8;
+constexpr int kIters = 2048;
+
+__global__ void fp64_fma_kernel(double seed, double* sink) {
+    double a[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) a[c] = seed + threadIdx.x * 1e-9 + c;
+    const double b = 0.999999999, d = 1e-12;
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) a[c] = fma(a[c], b, d);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += a[c];
+    if (s == 1234.5678) sink[0] = s;  // never true; keeps the chains live
+}
+
+}  // namespace
+}  // namespace rbg
+
+extern "C" rbg_status rbg_support_counts(rbg_ctx* ctx, const double* q, uint64_t nq,
+                                         uint64_t* sum_k, uint64_t* sum_k2) {
+    if (!ctx) return RBG_INVALID_ARGUMENT;
+    try {
+        if (!ctx->have_centres) throw rbg::Error(RBG_NOT_READY, "no reference points set");
+        RBG_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        ctx->ev_q.reserve(nq * ctx->dim + 1);
+        ctx->counters.reserve(4);
+        RBG_CUDA(cudaMemcpyAsync(ctx->ev_q.p, q, nq * ctx->dim * sizeof(double), cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemsetAsync(ctx->counters.p + 2, 0, 2 * sizeof(unsigned long long), st));
+        const rbg::GridDev g = rbg::grid_dev(ctx->grid);
+        const unsigned blocks = rbg::blocks_for(nq, 256);
+        if (ctx->dim == 2)
+            rbg::support_count_kernel<2><<<blocks, 256, 0, st>>>(g, ctx->tile_cptr.p, ctx->tile_cids.p,
+                                                                 ctx->centres.p, ctx->family, ctx->alpha,
+                                                                 ctx->r2, ctx->ev_q.p, nq, ctx->counters.p + 2);
+        else
+            rbg::support_count_kernel<3><<<blocks, 256, 0, st>>>(g, ctx->tile_cptr.p, ctx->tile_cids.p,
+                                                                 ctx->centres.p, ctx->family, ctx->alpha,
+                                                                 ctx->r2, ctx->ev_q.p, nq, ctx->counters.p + 2);
+        RBG_CHECK_LAUNCH(ctx);
+        unsigned long long h[2];
+        RBG_CUDA(cudaMemcpyAsync(h, ctx->counters.p + 2, sizeof(h), cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        *sum_k = h[0];
+        *sum_k2 = h[1];
+        return RBG_OK;
+    } catch (const rbg::Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    }
+}
+
+extern "C" rbg_status rbg_fp64_peak(rbg_ctx* ctx, double* tflops) {
+    if (!ctx || !tflops) return RBG_INVALID_ARGUMENT;
+    try {
+        RBG_CUDA(cudaSetDevice(ctx->device));
+        int sms = 0;
+        RBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        cudaStream_t st = ctx->stream;
+        ctx->counters.reserve(4);
+        const unsigned blocks = (unsigned)sms * 8u, threads = 256;
+        double best = 0.0;
+        for (int rep = 0; rep < 4; ++rep) {
+            RBG_CUDA(cudaEventRecord(ctx->ev0, st));
+            rbg::fp64_fma_kernel<<<blocks, threads, 0, st>>>(1.0 + rep, reinterpret_cast<double*>(ctx->counters.p));
+            RBG_CUDA(cudaEventRecord(ctx->ev1, st));
+            RBG_CUDA(cudaEventSynchronize(ctx->ev1));
+            float ms = 0.f;
+            RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+            const double flops = 2.0 * rbg::kChains * rbg::kIters * (double)blocks * threads;
+            if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        }
+        *tflops = best;
+        return RBG_OK;
+    } catch (const rbg::Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    }
+}
+
+extern "C" rbg_status rbg_assembly_times(rbg_ctx* ctx, double* bin_ms, double* tiles_ms) {
+    if (!ctx) return RBG_INVALID_ARGUMENT;
+    try {
+        RBG_CUDA(cudaSetDevice(ctx->device));
+        RBG_CUDA(cudaEventSynchronize(ctx->ev_asm[2]));
+        float a = 0.f, b = 0.f;
+        RBG_CUDA(cudaEventElapsedTime(&a, ctx->ev_asm[0], ctx->ev_asm[1]));
+        RBG_CUDA(cudaEventElapsedTime(&b, ctx->ev_asm[1], ctx->ev_asm[2]));
+        if (bin_ms) *bin_ms = a;
+        if (tiles_ms) *tiles_ms = b;
+        return RBG_OK;
+    } catch (const rbg::Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    }
+}

@@ -1,0 +1,436 @@
+// rbg_setup.cu -- K1 (centre binning) + K2 (symbolic pattern) for a centre set.
+//
+// Replaces what the reference does per assembly with radius queries
+// (assemble_submatrix, coo.cpp:166-192 over PointIndex, kdtree.cpp:57-87) and
+// the dense normal-matrix layout (solver.cpp:151-156):
+//   * a uniform tile grid over the centres' bounding box grown by the support
+//     radius 1/alpha; every tile gets the ascending list of centres whose
+//     support can reach it (a superset of every point-in-tile hit set);
+//   * the upper-triangle CSR pattern of A^T A: pairs i <= j with
+//     dist2(c_i, c_j) < (2/alpha)^2 (the predicate every co-supported pair
+//     satisfies), columns ascending; plus the symmetric full pattern and the
+//     full->upper slot map the solver uses;
+//   * per tile, the packed upper-triangle slot map local (a,b) -> offset of
+//     column c_b within upper row c_a, so the numeric kernel flushes its
+//     register tiles without searching.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "rbg_internal.cuh"
+
+namespace rbg {
+namespace {
+
+constexpr uint64_t kMaxTiles = 1ull << 25;
+constexpr double kTileMargin = 1e-6;  // relative, conservative rect growth
+
+struct TileTestDev {
+    GridDev g;
+    double edge, margin, r, lim;  // lim = r^2 (1 + 1e-6)
+};
+
+// Centres -> the tiles whose (grown) rectangle lies within the support radius.
+template <int DIM, bool FILL>
+__global__ void tile_lists_kernel(const double* __restrict__ c, uint64_t m, TileTestDev t,
+                                  uint32_t* __restrict__ count, const uint64_t* __restrict__ ptr,
+                                  uint32_t* __restrict__ ids) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double cc[3] = {c[i * DIM], c[i * DIM + 1], DIM == 3 ? c[i * DIM + 2] : 0.0};
+        const double lo[3] = {t.g.lo0, t.g.lo1, t.g.lo2};
+        const int64_t n[3] = {t.g.n0, t.g.n1, t.g.n2};
+        int64_t a0[3] = {0, 0, 0}, a1[3] = {0, 0, 0};
+        for (int d = 0; d < DIM; ++d) {
+            int64_t s = (int64_t)floor((cc[d] - t.r - lo[d]) / t.edge) - 1;
+            int64_t e = (int64_t)floor((cc[d] + t.r - lo[d]) / t.edge) + 1;
+            a0[d] = s < 0 ? 0 : s;
+            a1[d] = e >= n[d] ? n[d] - 1 : e;
+        }
+        for (int64_t iz = a0[2]; iz <= a1[2]; ++iz)
+            for (int64_t iy = a0[1]; iy <= a1[1]; ++iy)
+                for (int64_t ix = a0[0]; ix <= a1[0]; ++ix) {
+                    const int64_t idx[3] = {ix, iy, iz};
+                    double d2 = 0.0;
+                    for (int d = 0; d < DIM; ++d) {
+                        const double rlo = lo[d] + (double)idx[d] * t.edge - t.margin;
+                        const double rhi = lo[d] + (double)(idx[d] + 1) * t.edge + t.margin;
+                        const double gap = cc[d] < rlo ? rlo - cc[d] : (cc[d] > rhi ? cc[d] - rhi : 0.0);
+                        d2 += gap * gap;
+                    }
+                    if (d2 < t.lim) {
+                        const uint64_t tile = ((uint64_t)iz * (uint64_t)n[1] + (uint64_t)iy) *
+                                                  (uint64_t)n[0] +
+                                              (uint64_t)ix;
+                        const uint32_t k = atomicAdd(&count[tile], 1u);
+                        if (FILL) ids[ptr[tile] + k] = (uint32_t)i;
+                    }
+                }
+    }
+}
+
+// Full symmetric pattern rows: all j with dist2(c_i, c_j) < lim, via a host-
+// built cell grid of edge >= 2r (3^DIM neighbour cells).
+struct CellDev {
+    double lo0, lo1, lo2, inv_edge;
+    int64_t n0, n1, n2;
+};
+
+template <int DIM, bool FILL>
+__global__ void pattern_rows_kernel(const double* __restrict__ c, uint64_t m, CellDev g,
+                                    const uint64_t* __restrict__ cell_ptr,
+                                    const uint32_t* __restrict__ cell_ids, double lim,
+                                    uint32_t* __restrict__ row_len,
+                                    const uint64_t* __restrict__ fptr, uint32_t* __restrict__ fcols) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = c[i * DIM], y = c[i * DIM + 1], z = DIM == 3 ? c[i * DIM + 2] : 0.0;
+        const double lo[3] = {g.lo0, g.lo1, g.lo2};
+        const int64_t n[3] = {g.n0, g.n1, g.n2};
+        const double v[3] = {x, y, z};
+        int64_t a0[3] = {0, 0, 0}, a1[3] = {0, 0, 0};
+        for (int d = 0; d < DIM; ++d) {
+            int64_t cc = (int64_t)floor((v[d] - lo[d]) * g.inv_edge);
+            cc = cc < 0 ? 0 : (cc >= n[d] ? n[d] - 1 : cc);
+            a0[d] = cc - 1 < 0 ? 0 : cc - 1;
+            a1[d] = cc + 1 >= n[d] ? n[d] - 1 : cc + 1;
+        }
+        uint32_t k = 0;
+        const uint64_t base = FILL ? fptr[i] : 0;
+        for (int64_t iz = a0[2]; iz <= a1[2]; ++iz)
+            for (int64_t iy = a0[1]; iy <= a1[1]; ++iy)
+                for (int64_t ix = a0[0]; ix <= a1[0]; ++ix) {
+                    const uint64_t cell =
+                        ((uint64_t)iz * (uint64_t)n[1] + (uint64_t)iy) * (uint64_t)n[0] + (uint64_t)ix;
+                    for (uint64_t e = cell_ptr[cell]; e < cell_ptr[cell + 1]; ++e) {
+                        const uint32_t j = cell_ids[e];
+                        const double d2 = dist2_of<DIM>(x, y, z, c[(uint64_t)j * DIM],
+                                                        c[(uint64_t)j * DIM + 1],
+                                                        DIM == 3 ? c[(uint64_t)j * DIM + 2] : 0.0);
+                        if (d2 < lim) {
+                            if (FILL) fcols[base + k] = j;
+                            ++k;
+                        }
+                    }
+                }
+        if (!FILL) row_len[i] = k;
+    }
+}
+
+// Position of the diagonal in each sorted full row -> upper row length.
+__global__ void upper_len_kernel(const uint64_t* __restrict__ fptr,
+                                 const uint32_t* __restrict__ fcols, uint64_t m,
+                                 uint32_t* __restrict__ diag_pos, uint32_t* __restrict__ ulen) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = fptr[i], hi = fptr[i + 1];
+        const uint64_t b = lo, e = hi;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (fcols[mid] < (uint32_t)i) lo = mid + 1; else hi = mid;
+        }
+        diag_pos[i] = (uint32_t)(lo - b);
+        ulen[i] = (uint32_t)(e - lo);
+    }
+}
+
+__global__ void upper_fill_kernel(const uint64_t* __restrict__ fptr,
+                                  const uint32_t* __restrict__ fcols, uint64_t m,
+                                  const uint32_t* __restrict__ diag_pos,
+                                  const uint64_t* __restrict__ uptr, uint32_t* __restrict__ ucols) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t src = fptr[i] + diag_pos[i];
+        const uint64_t len = fptr[i + 1] - src;
+        for (uint64_t k = 0; k < len; ++k) ucols[uptr[i] + k] = fcols[src + k];
+    }
+}
+
+__device__ __forceinline__ uint64_t find_in_row(const uint32_t* cols, uint64_t lo, uint64_t hi,
+                                                uint32_t key) {
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (cols[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// full entry (i, j) -> upper slot of (min, max).
+__global__ void full_to_upper_kernel(const uint64_t* __restrict__ fptr,
+                                     const uint32_t* __restrict__ fcols, uint64_t m,
+                                     const uint32_t* __restrict__ diag_pos,
+                                     const uint64_t* __restrict__ uptr,
+                                     const uint32_t* __restrict__ ucols, uint64_t* __restrict__ f2u) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = fptr[i] + diag_pos[i];
+        for (uint64_t e = fptr[i]; e < fptr[i + 1]; ++e) {
+            const uint32_t j = fcols[e];
+            if (e >= d) {
+                f2u[e] = uptr[i] + (e - d);
+            } else {
+                f2u[e] = find_in_row(ucols, uptr[j], uptr[j + 1], (uint32_t)i);
+            }
+        }
+    }
+}
+
+// Per (tile, local row a): merge the tile's ascending list with upper row
+// c_a's ascending columns -> packed slot offsets.
+__global__ void tile_map_kernel(const uint64_t* __restrict__ cptr, uint64_t n_tiles,
+                                const uint32_t* __restrict__ cids, uint64_t total,
+                                const uint64_t* __restrict__ mptr, const uint64_t* __restrict__ uptr,
+                                const uint32_t* __restrict__ ucols, uint16_t* __restrict__ map) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        // tile = last t with cptr[t] <= e
+        uint64_t lo = 0, hi = n_tiles;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (cptr[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint64_t t = lo;
+        const uint64_t c0 = cptr[t];
+        const uint32_t L = (uint32_t)(cptr[t + 1] - c0);
+        const uint32_t a = (uint32_t)(e - c0);
+        const uint32_t ga = cids[e];
+        const uint64_t rb = uptr[ga], re = uptr[ga + 1];
+        uint64_t pos = rb;
+        uint16_t* out = map + mptr[t] + tri_index(a, a, L);
+        for (uint32_t b = a; b < L; ++b) {
+            const uint32_t gb = cids[c0 + b];
+            while (pos < re && ucols[pos] < gb) ++pos;
+            out[b - a] = (pos < re && ucols[pos] == gb) ? (uint16_t)(pos - rb) : (uint16_t)0xffff;
+        }
+    }
+}
+
+}  // namespace
+
+void setup_centres(rbg_ctx* ctx) {
+    const int dim = ctx->dim;
+    const uint64_t m = ctx->m;
+    cudaStream_t st = ctx->stream;
+
+    // ---- host: bounding box + tile grid plan ------------------------------
+    std::vector<double> hc(m * dim);
+    RBG_CUDA(cudaMemcpyAsync(hc.data(), ctx->centres.p, m * dim * sizeof(double),
+                             cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) lo[d] = hi[d] = hc[d];
+    for (uint64_t i = 0; i < m; ++i)
+        for (int d = 0; d < dim; ++d) {
+            lo[d] = std::min(lo[d], hc[i * dim + d]);
+            hi[d] = std::max(hi[d], hc[i * dim + d]);
+        }
+    const double r = ctx->radius;
+    TileGrid g;
+    g.dim = dim;
+    double edge = r / 4.0;
+    for (;;) {
+        uint64_t total = 1;
+        bool over = false;
+        for (int d = 0; d < 3; ++d) {
+            if (d < dim) {
+                g.lo[d] = lo[d] - r * (1.0 + 1e-7) - edge * 1e-3;
+                const double span = (hi[d] + r * (1.0 + 1e-7) + edge * 1e-3) - g.lo[d];
+                const double nd = std::max(1.0, std::ceil(span / edge));
+                if (nd > 1e9) over = true;
+                g.n[d] = (int64_t)nd;
+            } else {
+                g.lo[d] = 0.0;
+                g.n[d] = 1;
+            }
+            total *= (uint64_t)g.n[d];
+            if (total > kMaxTiles) over = true;
+        }
+        if (!over) {
+            g.count = total;
+            break;
+        }
+        edge *= 1.25;
+    }
+    g.edge = edge;
+    g.inv_edge = 1.0 / edge;
+    ctx->grid = g;
+    const uint64_t nt = g.count;
+
+    // ---- K1: tile centre lists ---------------------------------------------
+    ctx->tile_count.reserve(nt + 1);
+    ctx->tile_cptr.reserve(nt + 1);
+    RBG_CUDA(cudaMemsetAsync(ctx->tile_count.p, 0, (nt + 1) * sizeof(uint32_t), st));
+    TileTestDev tt{grid_dev(g), edge, edge * kTileMargin, r, ctx->r2 * (1.0 + 1e-6)};
+    const unsigned cb = blocks_for(m, 128);
+    if (dim == 2)
+        tile_lists_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
+                                                        nullptr, nullptr);
+    else
+        tile_lists_kernel<3, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
+                                                        nullptr, nullptr);
+    RBG_CHECK_LAUNCH(ctx);
+    exclusive_scan_u32_to_u64(ctx, ctx->tile_count.p, ctx->tile_cptr.p, nt);
+    std::vector<uint64_t> cptr(nt + 1);
+    RBG_CUDA(cudaMemcpyAsync(cptr.data(), ctx->tile_cptr.p, (nt + 1) * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    const uint64_t total_ids = cptr[nt];
+    ctx->tile_cids.reserve(std::max<uint64_t>(total_ids, 1));
+    RBG_CUDA(cudaMemsetAsync(ctx->tile_count.p, 0, (nt + 1) * sizeof(uint32_t), st));
+    if (dim == 2)
+        tile_lists_kernel<2, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
+                                                       ctx->tile_cptr.p, ctx->tile_cids.p);
+    else
+        tile_lists_kernel<3, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
+                                                       ctx->tile_cptr.p, ctx->tile_cids.p);
+    RBG_CHECK_LAUNCH(ctx);
+    uint32_t max_l = 0;
+    for (uint64_t t = 0; t < nt; ++t) max_l = std::max<uint32_t>(max_l, (uint32_t)(cptr[t + 1] - cptr[t]));
+    ctx->max_tile_centres = max_l;
+    segmented_sort_u32(ctx, ctx->tile_cids.p, ctx->tile_cptr.p, nt, max_l);
+
+    // ---- buckets + slot-map offsets (host) ----------------------------------
+    static const int kBuckets[] = {32, 48, 64, 80, 96, 128, 160};
+    std::vector<std::vector<uint32_t>> lists(std::size(kBuckets));
+    std::vector<uint32_t> fallback;
+    std::vector<uint64_t> mptr(nt + 1, 0);
+    for (uint64_t t = 0; t < nt; ++t) {
+        const uint64_t L = cptr[t + 1] - cptr[t];
+        mptr[t + 1] = mptr[t] + L * (L + 1) / 2;
+        if (L == 0) continue;
+        size_t b = 0;
+        while (b < std::size(kBuckets) && (uint64_t)kBuckets[b] < L) ++b;
+        if (b == std::size(kBuckets)) fallback.push_back((uint32_t)t);
+        else lists[b].push_back((uint32_t)t);
+    }
+    ctx->buckets.clear();
+    ctx->buckets.resize(std::size(kBuckets));
+    for (size_t b = 0; b < std::size(kBuckets); ++b) {
+        Bucket& bk = ctx->buckets[b];
+        bk.lb = kBuckets[b];
+        bk.n_tiles = lists[b].size();
+        if (bk.n_tiles) {
+            bk.tiles.reserve(bk.n_tiles);
+            RBG_CUDA(cudaMemcpyAsync(bk.tiles.p, lists[b].data(), bk.n_tiles * sizeof(uint32_t),
+                                     cudaMemcpyHostToDevice, st));
+        }
+    }
+    ctx->n_fallback = fallback.size();
+    if (!fallback.empty()) {
+        ctx->fallback_tiles.reserve(fallback.size());
+        RBG_CUDA(cudaMemcpyAsync(ctx->fallback_tiles.p, fallback.data(),
+                                 fallback.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    }
+    ctx->tile_mptr.reserve(nt + 1);
+    RBG_CUDA(cudaMemcpyAsync(ctx->tile_mptr.p, mptr.data(), (nt + 1) * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, st));
+
+    // ---- K2: pattern --------------------------------------------------------
+    const double two_r = 2.0 * r;
+    const double lim = two_r * two_r;
+    double cedge = two_r * (1.0 + 1e-9);
+    int64_t cn[3] = {1, 1, 1};
+    uint64_t ncell = 1;
+    for (;;) {
+        ncell = 1;
+        for (int d = 0; d < 3; ++d) {
+            cn[d] = d < dim ? (int64_t)std::floor((hi[d] - lo[d]) / cedge) + 1 : 1;
+            ncell *= (uint64_t)cn[d];
+        }
+        if (ncell <= std::max<uint64_t>(4 * m, 1u << 16)) break;
+        cedge *= 1.5;
+    }
+    const double cinv = 1.0 / cedge;
+    std::vector<uint64_t> cell_ptr(ncell + 1, 0);
+    std::vector<uint64_t> key(m);
+    for (uint64_t i = 0; i < m; ++i) {
+        uint64_t k = 0;
+        for (int d = dim - 1; d >= 0; --d) {
+            int64_t cc = (int64_t)std::floor((hc[i * dim + d] - lo[d]) * cinv);
+            cc = std::max<int64_t>(0, std::min<int64_t>(cn[d] - 1, cc));
+            k = k * (uint64_t)cn[d] + (uint64_t)cc;
+        }
+        key[i] = k;
+        ++cell_ptr[k + 1];
+    }
+    for (uint64_t cidx = 0; cidx < ncell; ++cidx) cell_ptr[cidx + 1] += cell_ptr[cidx];
+    std::vector<uint32_t> cell_ids(m);
+    {
+        std::vector<uint64_t> cur(cell_ptr.begin(), cell_ptr.end() - 1);
+        for (uint64_t i = 0; i < m; ++i) cell_ids[cur[key[i]]++] = (uint32_t)i;
+    }
+    DevBuf<uint64_t> d_cell_ptr;
+    DevBuf<uint32_t> d_cell_ids, d_len, d_diag;
+    d_cell_ptr.reserve(ncell + 1);
+    d_cell_ids.reserve(m);
+    d_len.reserve(m + 1);
+    d_diag.reserve(m);
+    RBG_CUDA(cudaMemcpyAsync(d_cell_ptr.p, cell_ptr.data(), (ncell + 1) * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, st));
+    RBG_CUDA(cudaMemcpyAsync(d_cell_ids.p, cell_ids.data(), m * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, st));
+    CellDev cd{lo[0], lo[1], lo[2], cinv, cn[0], cn[1], cn[2]};
+    ctx->fptr.reserve(m + 1);
+    if (dim == 2)
+        pattern_rows_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_cell_ptr.p,
+                                                          d_cell_ids.p, lim, d_len.p, nullptr, nullptr);
+    else
+        pattern_rows_kernel<3, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_cell_ptr.p,
+                                                          d_cell_ids.p, lim, d_len.p, nullptr, nullptr);
+    RBG_CHECK_LAUNCH(ctx);
+    exclusive_scan_u32_to_u64(ctx, d_len.p, ctx->fptr.p, m);
+    std::vector<uint64_t> hfptr(m + 1);
+    RBG_CUDA(cudaMemcpyAsync(hfptr.data(), ctx->fptr.p, (m + 1) * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    ctx->nnz_full = hfptr[m];
+    uint32_t max_row = 0;
+    for (uint64_t i = 0; i < m; ++i) max_row = std::max<uint32_t>(max_row, (uint32_t)(hfptr[i + 1] - hfptr[i]));
+    if (max_row >= 0xffff)
+        throw Error(RBG_INVALID_ARGUMENT, "pattern row of " + std::to_string(max_row) +
+                                              " centres exceeds the 65534-entry slot-map limit");
+    ctx->fcols.reserve(ctx->nnz_full);
+    if (dim == 2)
+        pattern_rows_kernel<2, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_cell_ptr.p,
+                                                         d_cell_ids.p, lim, nullptr, ctx->fptr.p,
+                                                         ctx->fcols.p);
+    else
+        pattern_rows_kernel<3, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_cell_ptr.p,
+                                                         d_cell_ids.p, lim, nullptr, ctx->fptr.p,
+                                                         ctx->fcols.p);
+    RBG_CHECK_LAUNCH(ctx);
+    segmented_sort_u32(ctx, ctx->fcols.p, ctx->fptr.p, m, max_row);
+    upper_len_kernel<<<cb, 128, 0, st>>>(ctx->fptr.p, ctx->fcols.p, m, d_diag.p, d_len.p);
+    RBG_CHECK_LAUNCH(ctx);
+    ctx->uptr.reserve(m + 1);
+    exclusive_scan_u32_to_u64(ctx, d_len.p, ctx->uptr.p, m);
+    RBG_CUDA(cudaMemcpyAsync(&ctx->nnz_upper, ctx->uptr.p + m, sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    ctx->ucols.reserve(ctx->nnz_upper);
+    upper_fill_kernel<<<cb, 128, 0, st>>>(ctx->fptr.p, ctx->fcols.p, m, d_diag.p, ctx->uptr.p,
+                                          ctx->ucols.p);
+    RBG_CHECK_LAUNCH(ctx);
+    ctx->f2u.reserve(ctx->nnz_full);
+    full_to_upper_kernel<<<cb, 128, 0, st>>>(ctx->fptr.p, ctx->fcols.p, m, d_diag.p, ctx->uptr.p,
+                                             ctx->ucols.p, ctx->f2u.p);
+    RBG_CHECK_LAUNCH(ctx);
+
+    // ---- per-tile slot maps -------------------------------------------------
+    ctx->tile_map.reserve(std::max<uint64_t>(mptr[nt], 1));
+    if (total_ids > 0) {
+        tile_map_kernel<<<blocks_for(total_ids, 256), 256, 0, st>>>(
+            ctx->tile_cptr.p, nt, ctx->tile_cids.p, total_ids, ctx->tile_mptr.p, ctx->uptr.p,
+            ctx->ucols.p, ctx->tile_map.p);
+        RBG_CHECK_LAUNCH(ctx);
+    }
+
+    // ---- system + point workspace sized for this centre set ----------------
+    ctx->sys.reserve(ctx->nnz_upper + 2 * m);
+    ctx->tile_pptr.reserve(nt + 1);
+    ctx->counters.reserve(4);
+    RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace rbg

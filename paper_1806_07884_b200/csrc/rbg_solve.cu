@@ -1,0 +1,360 @@
+// rbg_solve.cu -- K4: SPD solve of the assembled normal equations.
+//
+// Replaces solve_weights (solver.cpp:289-330).  The reference factors the
+// dense M x M matrix with Eigen LLT, which is infeasible beyond M ~ 5e4 (the
+// dense b alone is 8 TB at M = 1e6).  Here: Jacobi-preconditioned conjugate
+// gradients on the symmetric CSR matrix, hand-written fp64 kernels:
+//   spmv_dot   q = (B + shift I) p, fused with the p.q reduction
+//   update     x += a p, r -= a q, z = D^-1 r, fused with r.z and r.r
+//   direction  p = z + b p
+// Scalars (alpha, beta, convergence) live on the device; reductions finish in
+// the last block to arrive (fixed-order, so runs are deterministic) and the
+// iteration loop is replayed from a CUDA graph in batches, with one host
+// read of the convergence flags per batch.  Stopping rule:
+// ||r||_2 <= tol ||b||_2.  The reference's ridge ladder (solver.cpp:296-315)
+// is kept: lambda x trace/side is added on breakdown / non-convergence.
+#include <cmath>
+
+#include "rbg_internal.cuh"
+
+namespace rbg {
+namespace {
+
+// scalar slots
+enum : int {
+    S_RZ = 0,
+    S_PQ,
+    S_RR,
+    S_BB,
+    S_ALPHA,
+    S_BETA,
+    S_SHIFT,
+    S_STOP,
+    S_DONE,
+    S_FAIL,
+    S_ITERS,
+    S_MAXIT,
+    S_TRACE,
+    S_COUNT
+};
+
+constexpr int kThreads = 256;
+constexpr int kBatch = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block sum of up to two values -> partials[0*grid + b], partials[1*grid + b];
+// returns true in every thread of the last block to finish, after which
+// out0/out1 hold the grand totals (fixed reduction order).
+template <int NV>
+__device__ bool last_block_sum(const double (&v)[NV], double* partials, unsigned* ticket,
+                               double (&out)[NV]) {
+    __shared__ double sh[NV][kThreads / 32];
+    __shared__ bool is_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const double s = warp_sum(v[k]);
+        if (lane == 0) sh[k][warp] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) s += sh[k][w];
+            partials[k * gridDim.x + blockIdx.x] = s;
+        }
+        __threadfence();
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double s = 0.0;
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads)
+            s += ((volatile double*)partials)[k * gridDim.x + b];
+        s = warp_sum(s);
+        __syncthreads();
+        if (lane == 0) sh[k][warp] = s;
+        __syncthreads();
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) t += sh[k][w];
+        out[k] = t;
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+    return true;
+}
+
+__global__ void gather_full_kernel(const uint64_t* __restrict__ f2u, const double* __restrict__ uvals,
+                                   uint64_t nnz, double* __restrict__ vfull) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (uint64_t)gridDim.x * blockDim.x)
+        vfull[e] = uvals[f2u[e]];
+}
+
+__global__ void trace_kernel(const uint64_t* __restrict__ uptr, const double* __restrict__ uvals,
+                             uint64_t m, double* partials, unsigned* ticket, double* scal) {
+    double v[1] = {0.0};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        v[0] += uvals[uptr[i]];
+    double out[1];
+    if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) scal[S_TRACE] = out[0];
+}
+
+__global__ void init_kernel(const uint64_t* __restrict__ uptr, const double* __restrict__ uvals,
+                            const double* __restrict__ b, uint64_t m, double* __restrict__ dinv,
+                            double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+                            double* __restrict__ p, double* partials, unsigned* ticket, double* scal,
+                            double tol2) {
+    const double shift = scal[S_SHIFT];
+    double v[3] = {0.0, 0.0, 0.0};  // rz, bb, non-positive diagonal count
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double d = uvals[uptr[i]] + shift;  // upper row i starts at the diagonal
+        if (!(d > 0.0) || !isfinite(d)) v[2] += 1.0;
+        const double di = 1.0 / d;
+        dinv[i] = di;
+        const double bi = b[i];
+        x[i] = 0.0;
+        r[i] = bi;
+        const double zi = bi * di;
+        z[i] = zi;
+        p[i] = zi;
+        v[0] += bi * zi;
+        v[1] += bi * bi;
+    }
+    double out[3];
+    if (last_block_sum<3>(v, partials, ticket, out) && threadIdx.x == 0) {
+        scal[S_RZ] = out[0];
+        scal[S_BB] = out[1];
+        scal[S_STOP] = tol2 * out[1];
+        scal[S_ITERS] = 0.0;
+        scal[S_FAIL] = out[2] > 0.0 ? 1.0 : 0.0;
+        scal[S_DONE] = out[1] == 0.0 ? 1.0 : 0.0;
+        scal[S_RR] = out[1];
+    }
+}
+
+// q = (B + shift I) p, one warp per row; pq = p.q.
+__global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
+                                const double* __restrict__ vfull, uint64_t m,
+                                const double* __restrict__ p, double* __restrict__ q,
+                                double* partials, unsigned* ticket, double* scal) {
+    if (scal[S_DONE] != 0.0 || scal[S_FAIL] != 0.0) return;
+    const double shift = scal[S_SHIFT];
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
+    double v[1] = {0.0};
+    for (uint64_t row = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < m;
+         row += warps) {
+        double s = 0.0;
+        const uint64_t e1 = fptr[row + 1];
+        for (uint64_t e = fptr[row] + lane; e < e1; e += 32) s = fma(vfull[e], p[fcols[e]], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            const double pi = p[row];
+            const double qi = s + shift * pi;
+            q[row] = qi;
+            v[0] += pi * qi;
+        }
+    }
+    double out[1];
+    if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) {
+        const double pq = out[0];
+        scal[S_PQ] = pq;
+        if (!(pq > 0.0) || !isfinite(pq)) scal[S_FAIL] = 1.0;
+        else scal[S_ALPHA] = scal[S_RZ] / pq;
+    }
+}
+
+__global__ void update_kernel(uint64_t m, const double* __restrict__ p, const double* __restrict__ q,
+                              const double* __restrict__ dinv, double* __restrict__ x,
+                              double* __restrict__ r, double* __restrict__ z, double* partials,
+                              unsigned* ticket, double* scal) {
+    if (scal[S_DONE] != 0.0 || scal[S_FAIL] != 0.0) return;
+    const double a = scal[S_ALPHA];
+    double v[2] = {0.0, 0.0};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        x[i] += a * p[i];
+        const double ri = r[i] - a * q[i];
+        r[i] = ri;
+        const double zi = ri * dinv[i];
+        z[i] = zi;
+        v[0] += ri * zi;
+        v[1] += ri * ri;
+    }
+    double out[2];
+    if (last_block_sum<2>(v, partials, ticket, out) && threadIdx.x == 0) {
+        const double rz_new = out[0];
+        scal[S_BETA] = rz_new / scal[S_RZ];
+        scal[S_RZ] = rz_new;
+        scal[S_RR] = out[1];
+        const double it = scal[S_ITERS] + 1.0;
+        scal[S_ITERS] = it;
+        if (!isfinite(out[1])) scal[S_FAIL] = 1.0;
+        else if (out[1] <= scal[S_STOP]) scal[S_DONE] = 1.0;
+        else if (it >= scal[S_MAXIT]) scal[S_FAIL] = 2.0;
+    }
+}
+
+__global__ void direction_kernel(uint64_t m, const double* __restrict__ z, double* __restrict__ p,
+                                 const double* scal) {
+    if (scal[S_DONE] != 0.0 || scal[S_FAIL] != 0.0) return;
+    const double b = scal[S_BETA];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = z[i] + b * p[i];
+}
+
+// r = b - (B + shift I) x ; returns ||r||^2 in scal[S_PQ] (reused slot)
+__global__ void residual_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
+                                const double* __restrict__ vfull, uint64_t m,
+                                const double* __restrict__ x, const double* __restrict__ b,
+                                double* partials, unsigned* ticket, double* scal) {
+    const double shift = scal[S_SHIFT];
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
+    double v[1] = {0.0};
+    for (uint64_t row = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < m;
+         row += warps) {
+        double s = 0.0;
+        for (uint64_t e = fptr[row] + lane; e < fptr[row + 1]; e += 32) s = fma(vfull[e], x[fcols[e]], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            const double ri = b[row] - (s + shift * x[row]);
+            v[0] += ri * ri;
+        }
+    }
+    double out[1];
+    if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) scal[S_PQ] = out[0];
+}
+
+}  // namespace
+
+void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rbg_solve_diag* diag) {
+    cudaStream_t st = ctx->stream;
+    const uint64_t m = ctx->m, nnz = ctx->nnz_full;
+    const double tol = (opts && opts->tol > 0.0) ? opts->tol : 1e-12;
+    const int max_iter = (opts && opts->max_iter > 0) ? opts->max_iter : 20000;
+    const double* uvals = ctx->sys.p;
+    const double* b = ctx->sys.p + ctx->nnz_upper;
+
+    ctx->vfull.reserve(nnz);
+    for (auto* v : {&ctx->x, &ctx->r, &ctx->z, &ctx->p, &ctx->q, &ctx->dinv}) v->reserve(m);
+    const unsigned g_vec = blocks_for(m, kThreads, 148u * 4u);
+    const unsigned g_spmv = blocks_for(m, kThreads / 32, 148u * 8u);
+    const unsigned g_max = std::max(g_vec, g_spmv);
+    ctx->partials.reserve(3ull * g_max);
+    ctx->scal.reserve(S_COUNT);
+    ctx->ticket.reserve(1);
+    RBG_CUDA(cudaMemsetAsync(ctx->ticket.p, 0, sizeof(unsigned), st));
+    RBG_CUDA(cudaMemsetAsync(ctx->scal.p, 0, S_COUNT * sizeof(double), st));
+
+    RBG_CUDA(cudaEventRecord(ctx->ev0, st));
+    gather_full_kernel<<<blocks_for(nnz, kThreads), kThreads, 0, st>>>(ctx->f2u.p, uvals, nnz,
+                                                                        ctx->vfull.p);
+    RBG_CHECK_LAUNCH(ctx);
+    trace_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, m, ctx->partials.p, ctx->ticket.p,
+                                             ctx->scal.p);
+    RBG_CHECK_LAUNCH(ctx);
+    double trace = 0.0;
+    RBG_CUDA(cudaMemcpyAsync(&trace, ctx->scal.p + S_TRACE, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    const double mean_diag = trace / (double)m;  // solver.cpp:296
+
+    // one batch of iterations as a graph (kernels read their scalars on device)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    RBG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int it = 0; it < kBatch; ++it) {
+        spmv_dot_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m,
+                                                     ctx->p.p, ctx->q.p, ctx->partials.p,
+                                                     ctx->ticket.p, ctx->scal.p);
+        update_kernel<<<g_vec, kThreads, 0, st>>>(m, ctx->p.p, ctx->q.p, ctx->dinv.p, ctx->x.p,
+                                                  ctx->r.p, ctx->z.p, ctx->partials.p,
+                                                  ctx->ticket.p, ctx->scal.p);
+        direction_kernel<<<g_vec, kThreads, 0, st>>>(m, ctx->z.p, ctx->p.p, ctx->scal.p);
+    }
+    RBG_CUDA(cudaStreamEndCapture(st, &graph));
+    RBG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+
+    static const double kLambdas[] = {0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6};  // solver.cpp:298
+    rbg_solve_diag local{};
+    bool solved = false;
+    double flags[3] = {0, 0, 0};
+    try {
+        for (const double lambda : kLambdas) {
+            ++local.attempts;
+            const double shift = lambda * mean_diag;
+            const double init[2] = {shift, (double)max_iter};
+            RBG_CUDA(cudaMemcpyAsync(ctx->scal.p + S_SHIFT, &init[0], sizeof(double),
+                                     cudaMemcpyHostToDevice, st));
+            RBG_CUDA(cudaMemcpyAsync(ctx->scal.p + S_MAXIT, &init[1], sizeof(double),
+                                     cudaMemcpyHostToDevice, st));
+            init_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, b, m, ctx->dinv.p, ctx->x.p,
+                                                    ctx->r.p, ctx->z.p, ctx->p.p, ctx->partials.p,
+                                                    ctx->ticket.p, ctx->scal.p, tol * tol);
+            RBG_CHECK_LAUNCH(ctx);
+            for (;;) {
+                RBG_CUDA(cudaMemcpyAsync(flags, ctx->scal.p + S_DONE, 3 * sizeof(double),
+                                         cudaMemcpyDeviceToHost, st));
+                RBG_CUDA(cudaStreamSynchronize(st));
+                if (flags[0] != 0.0 || flags[1] != 0.0) break;
+                RBG_CUDA(cudaGraphLaunch(exec, st));
+                ctx->launches += 3 * kBatch;
+            }
+            if (flags[0] != 0.0 && flags[1] == 0.0) {
+                solved = true;
+                local.ridge_lambda = lambda;
+                local.ridge_shift = shift;
+                local.iterations = (int)flags[2];
+                break;
+            }
+        }
+    } catch (...) {
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        throw;
+    }
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (!solved) {
+        // first non-positive diagonal (the pivot an LLT meets first on an
+        // empty-support column), else the last row reached.
+        std::vector<double> dg(m);
+        RBG_CUDA(cudaMemcpyAsync(dg.data(), ctx->dinv.p, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        uint64_t piv = 0;
+        while (piv < m && dg[piv] > 0.0 && std::isfinite(dg[piv])) ++piv;
+        if (piv == m) piv = 0;
+        throw Error(RBG_RUNTIME_ERROR,
+                    "normal system is not positive definite even with ridge 1e-06; first "
+                    "non-positive pivot at index " + std::to_string(piv));
+    }
+    residual_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, ctx->x.p,
+                                                 b, ctx->partials.p, ctx->ticket.p, ctx->scal.p);
+    RBG_CHECK_LAUNCH(ctx);
+    RBG_CUDA(cudaEventRecord(ctx->ev1, st));
+    double rr_true = 0.0, bb = 0.0;
+    RBG_CUDA(cudaMemcpyAsync(&rr_true, ctx->scal.p + S_PQ, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaMemcpyAsync(&bb, ctx->scal.p + S_BB, sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (c_out)
+        RBG_CUDA(cudaMemcpyAsync(c_out, ctx->x.p, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    local.solve_ms = ms;
+    local.rel_residual = bb > 0.0 ? std::sqrt(rr_true / bb) : 0.0;
+    if (diag) *diag = local;
+}
+
+}  // namespace rbg

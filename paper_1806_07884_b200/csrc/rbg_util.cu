@@ -1,0 +1,176 @@
+// rbg_util.cu -- exclusive scans and a warp-per-segment bitonic sort used by
+// the binning (counting sort) and symbolic (pattern) phases.
+#include "rbg_internal.cuh"
+
+namespace rbg {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanChunk = kScanThreads * kScanItems;
+
+template <typename In>
+__device__ __forceinline__ uint64_t load_val(const In* p, uint64_t i, uint64_t n) {
+    return i < n ? (uint64_t)p[i] : 0ull;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive
+// prefix and writes the block total to *total.
+__device__ __forceinline__ uint64_t block_exclusive(uint64_t v, uint64_t* total) {
+    __shared__ uint64_t warp_sums[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t s = lane < kScanThreads / 32 ? warp_sums[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += t;
+        }
+        if (lane < kScanThreads / 32) warp_sums[lane] = s;  // inclusive
+    }
+    __syncthreads();
+    const uint64_t warp_off = warp == 0 ? 0ull : warp_sums[warp - 1];
+    *total = warp_sums[kScanThreads / 32 - 1];
+    __syncthreads();
+    return warp_off + incl - v;
+}
+
+template <typename In>
+__global__ void scan_block_sums(const In* in, uint64_t n, uint64_t* sums) {
+    const uint64_t base = (uint64_t)blockIdx.x * kScanChunk + threadIdx.x * kScanItems;
+    uint64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) s += load_val(in, base + k, n);
+    uint64_t total;
+    block_exclusive(s, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// Single-block exclusive scan of the block sums (any length, chunked with carry).
+__global__ void scan_sums_inplace(uint64_t* sums, uint64_t nb) {
+    uint64_t carry = 0;
+    for (uint64_t c0 = 0; c0 < nb; c0 += kScanChunk) {
+        const uint64_t base = c0 + threadIdx.x * kScanItems;
+        uint64_t v[kScanItems];
+        uint64_t s = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            v[k] = base + k < nb ? sums[base + k] : 0ull;
+            s += v[k];
+        }
+        uint64_t total;
+        uint64_t ex = block_exclusive(s, &total) + carry;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < nb) sums[base + k] = ex;
+            ex += v[k];
+        }
+        carry += total;
+    }
+}
+
+template <typename In>
+__global__ void scan_apply(const In* in, uint64_t n, const uint64_t* sums, uint64_t* out) {
+    const uint64_t base = (uint64_t)blockIdx.x * kScanChunk + threadIdx.x * kScanItems;
+    uint64_t v[kScanItems];
+    uint64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = load_val(in, base + k, n);
+        s += v[k];
+    }
+    uint64_t total;
+    uint64_t ex = block_exclusive(s, &total) + sums[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k <= n) out[base + k] = ex;  // out has n+1 entries: out[n] = total
+        ex += v[k];
+    }
+}
+
+template <typename In>
+void exclusive_scan_impl(rbg_ctx* ctx, const In* in, uint64_t* out, uint64_t n) {
+    // out[0..n] (n+1 entries); out[n] = sum.
+    const uint64_t nb = (n + 1 + kScanChunk - 1) / kScanChunk;
+    ctx->scan_tmp.reserve(nb);
+    scan_block_sums<In><<<(unsigned)nb, kScanThreads, 0, ctx->stream>>>(in, n, ctx->scan_tmp.p);
+    RBG_CHECK_LAUNCH(ctx);
+    scan_sums_inplace<<<1, kScanThreads, 0, ctx->stream>>>(ctx->scan_tmp.p, nb);
+    RBG_CHECK_LAUNCH(ctx);
+    scan_apply<In><<<(unsigned)nb, kScanThreads, 0, ctx->stream>>>(in, n, ctx->scan_tmp.p, out);
+    RBG_CHECK_LAUNCH(ctx);
+}
+
+// One warp per segment: load into shared memory padded with UINT32_MAX to a
+// power of two, bitonic sort, write back.
+__global__ void segsort_warp(uint32_t* keys, const uint64_t* seg_ptr, uint64_t n_segs, int p2) {
+    extern __shared__ uint32_t sm[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    uint32_t* s = sm + (size_t)wib * p2;
+    const uint64_t warps_total = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t seg = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; seg < n_segs;
+         seg += warps_total) {
+        const uint64_t b = seg_ptr[seg];
+        const int len = (int)(seg_ptr[seg + 1] - b);
+        if (len <= 1) continue;
+        int n2 = 32;
+        while (n2 < len) n2 <<= 1;
+        for (int i = lane; i < n2; i += 32) s[i] = i < len ? keys[b + i] : 0xffffffffu;
+        __syncwarp();
+        for (int k = 2; k <= n2; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < n2; i += 32) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const uint32_t a = s[i], c = s[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((a > c) == up) {
+                            s[i] = c;
+                            s[ixj] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int i = lane; i < len; i += 32) keys[b + i] = s[i];
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+void exclusive_scan_u32_to_u64(rbg_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n) {
+    exclusive_scan_impl<uint32_t>(ctx, in, out, n);
+}
+
+void exclusive_scan_u64(rbg_ctx* ctx, const uint64_t* in, uint64_t* out, uint64_t n) {
+    exclusive_scan_impl<uint64_t>(ctx, in, out, n);
+}
+
+void segmented_sort_u32(rbg_ctx* ctx, uint32_t* keys, const uint64_t* seg_ptr, uint64_t n_segs,
+                        uint32_t max_len) {
+    if (n_segs == 0 || max_len <= 1) return;
+    int p2 = 32;
+    while ((uint32_t)p2 < max_len) p2 <<= 1;
+    if (p2 > 4096)
+        throw Error(RBG_INVALID_ARGUMENT,
+                    "support neighbourhood too large: a segment holds " + std::to_string(max_len) +
+                        " centres (limit 4096); reduce the support radius");
+    const int warps = p2 >= 2048 ? 2 : 4;
+    const size_t smem = (size_t)warps * p2 * sizeof(uint32_t);
+    const uint64_t blocks = (n_segs + warps - 1) / warps;
+    segsort_warp<<<(unsigned)(blocks > 148u * 128u ? 148u * 128u : blocks), warps * 32, smem,
+                   ctx->stream>>>(keys, seg_ptr, n_segs, p2);
+    RBG_CHECK_LAUNCH(ctx);
+}
+
+}  // namespace rbg

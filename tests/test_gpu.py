@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle and the
+reference's own golden outputs.
+
+Tolerances (north_star): pattern bit-exact; A^T A / A^T h within 1e-10 using
+the reference's scale-normalised metric max|d|/max|ref| (acceptance_main.cpp:
+118-125), B additionally elementwise (all B terms are >= 0, no cancellation);
+hits / design_nnz exact; evaluation bit-exact for the same c; c within 1e-8.
+"""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+from paper_1806_07884_b200 import api, configs
+
+pytestmark = pytest.mark.gpu
+
+TOL_SYS = 1e-10
+TOL_C = 1e-8
+
+
+def scaled(a, b):
+    s = np.max(np.abs(b)) if b.size else 0.0
+    return float(np.max(np.abs(a - b)) / s) if s > 0 else float(np.max(np.abs(a - b), initial=0.0))
+
+
+def elementwise(a, b):
+    d = np.abs(a - b)
+    m = np.maximum(np.abs(a), np.abs(b))
+    return float(np.max(np.where(m > 0, d / np.where(m > 0, m, 1.0), 0.0), initial=0.0))
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = api.Engine(0)
+    yield e
+    e.close()
+
+
+def run_and_compare(eng, pts, h, refs, family, alpha, accumulate_slabs=1):
+    k = api.KernelSpec(family, alpha)
+    eng.set_centres(refs, k)
+    if accumulate_slabs == 1:
+        eng.assemble(pts, h)
+    else:
+        parts = np.array_split(np.arange(len(h)), accumulate_slabs)
+        for i, idx in enumerate(parts):
+            eng.assemble(pts[idx], h[idx], accumulate=i > 0)
+    rp, cols = eng.pattern()
+    orp, ocols = po.pattern(refs, alpha)
+    assert np.array_equal(rp, orp), "row_ptr differs"
+    assert np.array_equal(cols, ocols), "cols differ"
+    s = eng.system()
+    ov, orhs, ohits = po.assemble(pts, h, refs, k.family, alpha, orp, ocols)
+    assert scaled(s["values"], ov) < TOL_SYS
+    assert elementwise(s["values"], ov) < TOL_SYS
+    assert scaled(s["rhs"], orhs) < TOL_SYS
+    assert np.array_equal(s["hits"].astype(np.uint64), ohits)
+    assert s["design_nnz"] == int(ohits.sum())
+    return s, (orp, ocols, ov, orhs, ohits)
+
+
+# ------------------------------------------------------------- golden pins
+def test_readme_case_vs_reference(eng, golden):
+    g = golden("readme_case")
+    s, (rp, cols, ov, orhs, _) = run_and_compare(eng, g["points"], g["values"], g["refs"], 1, 0.5)
+    dense = api.SparseNormalSystem(81, rp, cols, s["values"], s["rhs"], np.array([]), 0).to_dense()
+    assert scaled(dense, g["b"]) < TOL_SYS and scaled(s["rhs"], g["rhs"]) < TOL_SYS
+    assert s["design_nnz"] == int(g["published_design_nnz"]) == 88209
+    f = eng.evaluate(g["c"], g["points"])
+    assert np.array_equal(f, g["f"])  # bitwise vs the reference's evaluate_model
+
+
+def test_small_instances_vs_reference(eng, golden):
+    g = golden("random_small")
+    for k in range(int(g["count"])):
+        s, (rp, cols, *_r) = run_and_compare(eng, g[f"{k}_points"], g[f"{k}_values"], g[f"{k}_refs"],
+                                             int(g[f"{k}_family"]), float(g[f"{k}_alpha"]))
+        m = len(g[f"{k}_refs"])
+        dense = api.SparseNormalSystem(m, rp, cols, s["values"], s["rhs"], np.array([]), 0).to_dense()
+        assert scaled(dense, g[f"{k}_b"]) < TOL_SYS
+        assert np.array_equal(s["hits"].astype(np.uint32), g[f"{k}_ref_nnz"])
+
+
+def test_cfg1_full_vs_reference(eng, golden):
+    g = golden("cfg1_system")
+    xy, h = configs.points("cfg1")
+    refs = configs.centres("cfg1")
+    s, (rp, cols, ov, orhs, _) = run_and_compare(eng, xy, h, refs, 1, float(g["alpha"]))
+    assert len(cols) == 50898 and s["design_nnz"] == int(g["design_nnz"])
+    c, diag = eng.solve()
+    assert diag["ridge_lambda"] == 0.0 and diag["rel_residual"] < 1e-11
+    assert np.max(np.abs(c - g["c"])) / np.max(np.abs(g["c"])) < TOL_C  # vs reference-path Cholesky
+    f = eng.evaluate(c, xy[:5000])
+    assert np.array_equal(f, po.evaluate(refs, c, 1, float(g["alpha"]), xy[:5000]))
+    rep = eng.error_report(c, xy, h)
+    assert rep["mean_absolute_error"] == pytest.approx(float(g["mae"]), rel=1e-6)
+
+
+# ------------------------------------------------------------ configs
+@pytest.mark.parametrize("name,n", [("cfg2", 100_000), ("cfg3", 60_000), ("cfg4", 200_000)])
+def test_config_subsamples(eng, name, n):
+    cfg = configs.CONFIGS[name]
+    xy, h = configs.points(name, n=n)
+    refs = configs.centres(name)
+    if name == "cfg3":
+        refs = refs[:6000]  # keeps the oracle's run in seconds; same density class
+    run_and_compare(eng, xy, h, refs, api.KERNELS[cfg.kernel], cfg.alpha if name != "cfg3" else cfg.alpha / 2)
+
+
+def test_slab_accumulation_equals_single(eng):
+    xy, h = configs.points("cfg2", n=50_000)
+    refs = configs.centres("cfg2")
+    run_and_compare(eng, xy, h, refs, 1, configs.CONFIGS["cfg2"].alpha, accumulate_slabs=4)
+
+
+def test_fallback_tiles_dense_centres(eng):
+    # centre lists above the largest register tile (160) take the slow path
+    rng = np.random.default_rng(11)
+    refs = rng.random((400, 2)) * 0.2
+    pts = rng.random((3000, 2)) * 0.3
+    h = rng.standard_normal(3000)
+    eng.set_centres(refs, api.KernelSpec("wendland-3-1", 8.0))
+    assert eng.pattern_info()["n_fallback"] > 0
+    run_and_compare(eng, pts, h, refs, 1, 8.0)
+
+
+@pytest.mark.parametrize("family", [0, 1, 2, 3])
+def test_all_families_3d_and_2d(eng, family):
+    rng = np.random.default_rng(family)
+    for dim in (2, 3):
+        refs = rng.random((300, dim))
+        pts = rng.random((5000, dim))
+        h = rng.standard_normal(5000)
+        run_and_compare(eng, pts, h, refs, family, 4.0)
+
+
+# ------------------------------------------------------------- edges
+def test_edge_cases(eng):
+    k = api.KernelSpec("wendland-3-0", 1.0)
+    # one point, one centre: fit degenerates to c = 5 (test_solver.cpp:353-367)
+    eng.set_centres(np.array([[0.0, 0.0]]), k)
+    eng.assemble(np.array([[0.0, 0.0]]), np.array([5.0]))
+    c, _ = eng.solve()
+    assert c[0] == pytest.approx(5.0, rel=1e-14)
+    assert eng.evaluate(c, np.array([[0.0, 0.0]]))[0] == pytest.approx(5.0, rel=1e-14)
+    # empty input, points outside every support, duplicates
+    refs = np.array([[0.5, 0.5], [0.6, 0.5]])
+    eng.set_centres(refs, api.KernelSpec("wendland-3-1", 5.0))
+    eng.assemble(np.zeros((0, 2)), np.zeros(0))
+    assert not eng.system()["values"].any()
+    far = np.array([[10.0, 10.0], [-5.0, 0.5]])
+    pts = np.vstack([far, np.repeat([[0.55, 0.5]], 7, axis=0)])
+    h = np.arange(9.0)
+    run_and_compare(eng, pts, h, refs, 1, 5.0)
+    # strict support boundary: (3,4) at distance 5 with radius 5 is excluded (test_kdtree.cpp:28-38)
+    eng.set_centres(np.array([[0.0, 0.0]]), api.KernelSpec("wendland-3-0", 0.2))
+    eng.assemble(np.array([[3.0, 4.0], [0.0, 0.0]]), np.array([1.0, 1.0]))
+    assert eng.system()["hits"].tolist() == [1.0]
+
+
+def test_invalid_inputs(eng):
+    with pytest.raises(ValueError):
+        eng.set_centres(np.array([[0.0, np.nan]]), api.KernelSpec("wendland-3-1", 1.0))
+    eng.set_centres(np.array([[0.0, 0.0]]), api.KernelSpec("wendland-3-1", 1.0))
+    with pytest.raises(ValueError, match="index 1"):
+        eng.assemble(np.array([[0.0, 0.0], [np.inf, 0.0]]), np.zeros(2))
+
+
+def test_empty_support_ridge_and_pivot_message(eng):
+    rng = np.random.default_rng(5)
+    pts = rng.random((60, 2))
+    h = 2.0 * rng.random(60) - 1.0
+    refs = np.array([[0.1, 0.1], [0.9, 0.1], [0.1, 0.9], [0.9, 0.9], [50.0, 50.0]])
+    eng.set_centres(refs, api.KernelSpec("wendland-3-0", 1.0))
+    eng.assemble(pts, h)
+    assert eng.system()["hits"][4] == 0
+    c, diag = eng.solve()
+    assert diag["ridge_lambda"] > 0.0 and abs(c[4]) < 1e-8
+    eng.set_system(np.zeros(eng.pattern_info()["nnz_upper"]), np.ones(5))
+    with pytest.raises(RuntimeError, match="pivot"):
+        eng.solve()
+
+
+# ------------------------------------------------- full-size properties
+def test_cfg2_full_size_properties(eng):
+    """Size-independent checks at BASELINE config 2's full size:
+    x^T B x == ||A x||^2 (A x evaluated by the eval kernel), rhs == B c for
+    h = A c, and the solve recovers c."""
+    cfg = configs.CONFIGS["cfg2"]
+    xy, _ = configs.points("cfg2")
+    refs = configs.centres("cfg2")
+    k = api.KernelSpec(cfg.kernel, cfg.alpha)
+    eng.set_centres(refs, k)
+    rng = np.random.default_rng(7)
+    c_true = rng.standard_normal(cfg.m)
+    h = eng.evaluate(c_true, xy)  # h = A c_true exactly representable input
+    eng.assemble(xy, h)
+    s = eng.system()
+    rp, cols = eng.pattern()
+    B = api.SparseNormalSystem(cfg.m, rp, cols, s["values"], s["rhs"], np.array([]), 0)
+    import scipy.sparse as sp
+    rows = np.repeat(np.arange(cfg.m), np.diff(rp.astype(np.int64)))
+    U = sp.csr_matrix((s["values"], (rows, cols.astype(np.int64))), shape=(cfg.m, cfg.m))
+    Bs = U + sp.triu(U, 1).T
+    x = rng.standard_normal(cfg.m)
+    ax = eng.evaluate(x, xy)
+    assert float(x @ (Bs @ x)) == pytest.approx(float(ax @ ax), rel=1e-10)
+    assert scaled(Bs @ c_true, s["rhs"]) < 1e-10
+    assert s["design_nnz"] == int(s["hits"].sum())
+    c, diag = eng.solve()
+    assert np.max(np.abs(c - c_true)) / np.max(np.abs(c_true)) < 1e-7
+    del B
