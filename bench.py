@@ -203,7 +203,10 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream shared by torch and the engine, so the step
+    # events and NCCL are ordered with the engine's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     xy, h = configs.points(cfg.name, seed_offset=rank)
     refs = configs.centres(cfg.name)

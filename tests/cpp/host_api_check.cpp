@@ -1,0 +1,112 @@
+// Exercises the C++ host layer (paper_1806_07884_b200/csrc/rbfit_gpu.hpp) the
+// way the reference's callers use rbfit:: (solver.hpp / model.hpp).
+//   host_api_check cpu                 -- validation paths, no GPU touched
+//   host_api_check gpu <in.bin> <out.bin>
+// in.bin : u64 n, u64 m, f64 alpha, f64 xy[n*2], f64 h[n], f64 refs[m*2]
+// out.bin: u64 design_nnz, u64 n_empty, u64 nnz_upper, f64 mae, f64 dev, f64 c[m],
+//          f64 f_eval[n], f64 rhs[m], f64 diag[m]
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rbfit_gpu.hpp"
+
+using namespace rbfit_b200;
+
+static int failures = 0;
+#define EXPECT_THROW(stmt, T, needle)                                                   \
+    do {                                                                                \
+        try {                                                                           \
+            stmt;                                                                       \
+            std::printf("FAIL no throw: %s\n", #stmt);                                  \
+            ++failures;                                                                 \
+        } catch (const T& e) {                                                          \
+            if (std::string(e.what()).find(needle) == std::string::npos) {              \
+                std::printf("FAIL message '%s' lacks '%s'\n", e.what(), needle);        \
+                ++failures;                                                             \
+            }                                                                           \
+        } catch (const std::exception& e) {                                             \
+            std::printf("FAIL wrong exception for %s: %s\n", #stmt, e.what());          \
+            ++failures;                                                                 \
+        }                                                                               \
+    } while (0)
+
+static int cpu_checks() {
+    EXPECT_THROW(KernelSpec(KernelFamily::wendland_3_0, 0.0), std::invalid_argument, "positive");
+    EXPECT_THROW(KernelSpec(KernelFamily::wendland_3_0, std::nan("")), std::invalid_argument, "finite");
+    EXPECT_THROW(kernel_from_name("gaussian"), std::invalid_argument, "unknown kernel");
+    if (kernel_name(kernel_from_name("wendland-3-1")) != "wendland-3-1") ++failures;
+    const KernelSpec k(KernelFamily::wendland_3_1, 1.0);
+    if (k.evaluate(0.5) != 0.1875) ++failures;  // test_kernel.cpp:14
+    if (KernelSpec(KernelFamily::wendland_3_3, 1.0).evaluate(0.5) != 0.0595703125) ++failures;
+    EXPECT_THROW(k.evaluate(-1.0), std::domain_error, "radius");
+    PointCloud empty;
+    EXPECT_THROW(fit(empty, {{0.0, 0.0}}, k), std::invalid_argument, "empty point cloud");
+    PointCloud one;
+    one.points = {{0.0, 0.0}};
+    one.values = {1.0, 2.0};
+    EXPECT_THROW(fit(one, {{0.0, 0.0}}, k), std::invalid_argument, "value count mismatch");
+    one.values = {1.0};
+    EXPECT_THROW(fit(one, {}, k), std::invalid_argument, "no reference points");
+    FitOptions poly;
+    poly.poly = true;
+    EXPECT_THROW(fit(one, {{0.0, 0.0}}, k, poly), std::invalid_argument, "polynomial");
+    std::printf("cpu checks: %d failures\n", failures);
+    return failures;
+}
+
+static int gpu_run(const char* in_path, const char* out_path) {
+    std::ifstream in(in_path, std::ios::binary);
+    std::uint64_t n = 0, m = 0;
+    double alpha = 0;
+    in.read(reinterpret_cast<char*>(&n), 8);
+    in.read(reinterpret_cast<char*>(&m), 8);
+    in.read(reinterpret_cast<char*>(&alpha), 8);
+    PointCloud cloud;
+    cloud.points.resize(n);
+    cloud.values.resize(n);
+    std::vector<Point2> refs(m);
+    in.read(reinterpret_cast<char*>(cloud.points.data()), n * 16);
+    in.read(reinterpret_cast<char*>(cloud.values.data()), n * 8);
+    in.read(reinterpret_cast<char*>(refs.data()), m * 16);
+    const KernelSpec kernel(KernelFamily::wendland_3_1, alpha);
+
+    FitReport report;
+    const Model model = fit(cloud, refs, kernel, {}, &report);
+    const ErrorReport er = error_report(model, cloud, report.design_nnz);
+    const std::vector<double> f = evaluate_model(model, cloud.points);
+
+    Device dev(0);
+    BuildStats stats;
+    const NormalSystem sys = build_normal_system(cloud, refs, kernel, false, &stats, &dev);
+    SolveDiag sd;
+    const Weights w = solve_weights(sys, &sd, &dev);
+    double worst = 0.0;
+    for (std::size_t j = 0; j < m; ++j) worst = std::max(worst, std::abs(w.c[j] - model.weights[j]));
+
+    std::ofstream out(out_path, std::ios::binary);
+    const std::uint64_t hdr[3] = {report.design_nnz, report.empty_support_refs.size(), sys.values.size()};
+    out.write(reinterpret_cast<const char*>(hdr), sizeof hdr);
+    out.write(reinterpret_cast<const char*>(&er.mean_absolute_error), 8);
+    out.write(reinterpret_cast<const char*>(&er.deviation_of_error), 8);
+    out.write(reinterpret_cast<const char*>(model.weights.data()), m * 8);
+    out.write(reinterpret_cast<const char*>(f.data()), n * 8);
+    out.write(reinterpret_cast<const char*>(sys.rhs.data()), m * 8);
+    std::vector<double> diag(m);
+    for (std::size_t j = 0; j < m; ++j) diag[j] = sys.at(j, j);
+    out.write(reinterpret_cast<const char*>(diag.data()), m * 8);
+    std::printf("gpu run: design_nnz=%zu mae=%.17g two-path c diff=%.3g iters=%d\n", report.design_nnz,
+                er.mean_absolute_error, worst, report.iterations);
+    return std::isfinite(worst) ? 0 : 1;
+}
+
+int main(int argc, char** argv) {
+    if (argc >= 2 && std::strcmp(argv[1], "cpu") == 0) return cpu_checks();
+    if (argc >= 4 && std::strcmp(argv[1], "gpu") == 0) return gpu_run(argv[2], argv[3]);
+    std::fprintf(stderr, "usage: host_api_check cpu | gpu in.bin out.bin\n");
+    return 2;
+}

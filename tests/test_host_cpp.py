@@ -1,0 +1,54 @@
+"""The C++ host layer (rbfit_b200::fit & co.) driven from a C++ caller."""
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+PKG = ROOT / "paper_1806_07884_b200"
+
+
+@pytest.fixture(scope="module")
+def exe(tmp_path_factory):
+    out = tmp_path_factory.mktemp("cpp") / "host_api_check"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{PKG / 'csrc'}", f"-I{ROOT / 'include'}",
+                    str(ROOT / "tests" / "cpp" / "host_api_check.cpp"), "-o", str(out),
+                    f"-L{PKG}", "-lrbfit_b200", "-lrbg", f"-Wl,-rpath,{PKG}"], check=True)
+    return out
+
+
+def test_host_layer_validation_without_gpu(exe):
+    r = subprocess.run([str(exe), "cpu"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_host_layer_fit_matches_reference_golden(exe, tmp_path, golden):
+    g = golden("readme_case")
+    xy, h, refs = g["points"], g["values"], g["refs"]
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        np.array([len(h), len(refs)], dtype=np.uint64).tofile(f)
+        np.array([0.5]).tofile(f)
+        xy.astype(np.float64).tofile(f)
+        h.astype(np.float64).tofile(f)
+        refs.astype(np.float64).tofile(f)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), "gpu", str(inp), str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    raw = np.fromfile(out, dtype=np.uint8)
+    hdr = raw[:24].view(np.uint64)
+    dbl = raw[24:].view(np.float64)
+    m, n = len(refs), len(h)
+    mae, dev = dbl[0], dbl[1]
+    c = dbl[2:2 + m]
+    f = dbl[2 + m:2 + m + n]
+    rhs = dbl[2 + m + n:2 + 2 * m + n]
+    diag = dbl[2 + 2 * m + n:]
+    assert int(hdr[0]) == 88209 and int(hdr[1]) == 0
+    assert np.max(np.abs(rhs - g["rhs"])) / np.max(np.abs(g["rhs"])) < 1e-10
+    assert np.max(np.abs(diag - np.diag(g["b"]))) / np.max(np.diag(g["b"])) < 1e-10
+    # README.md:69 mae of this fit (ill-conditioned, alpha = 0.5: loose by design)
+    assert mae == pytest.approx(float(g["published_mae"]), rel=1e-4)
+    assert np.all(np.isfinite(f)) and np.all(np.isfinite(c))
