@@ -290,7 +290,7 @@ void setup_centres(rbg_ctx* ctx) {
     segmented_sort_u32(ctx, ctx->tile_cids.p, ctx->tile_cptr.p, nt, max_l);
 
     // ---- buckets + slot-map offsets (host) ----------------------------------
-    static const int kBuckets[] = {32, 48, 64, 80, 96, 128, 160};
+    static const int kBuckets[] = {16, 24, 32, 40, 48, 56, 64, 72, 80, 96, 112, 128, 160};
     std::vector<std::vector<uint32_t>> lists(std::size(kBuckets));
     std::vector<uint32_t> fallback;
     std::vector<uint64_t> mptr(nt + 1, 0);

@@ -1,0 +1,6 @@
+# usage: bash scripts/gpu_prof.sh TAG CONFIG KERNEL_REGEX -- plain bench run, then ncu --set full of the tile kernel
+TAG=${1:-p}; CFG=${2:-cfg2}; KRX=${3:-assemble_tiles}
+CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-fit --e2e-steps 1 --config $CFG"
+timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$KRX" -s 1 -c 1 -o gpurun_out/${TAG}_prof $CMD > gpurun_out/${TAG}_ncu.log 2>&1
+echo "rc=$?" >> gpurun_out/${TAG}_plain.log
