@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--tile-div", type=float, default=None, help="tile edge = radius / this")
     return ap.parse_args()
 
 
@@ -212,6 +213,8 @@ def run_ours(args, cfg):
     refs = configs.centres(cfg.name)
     kernel = api.KernelSpec(cfg.kernel, cfg.alpha)
     eng = api.Engine(local, stream=stream.cuda_stream)
+    if args.tile_div:
+        eng.set_tile_divisor(args.tile_div)
     eng.set_centres(refs, kernel)
     info = eng.pattern_info()
     d_xy = torch.from_numpy(xy).cuda()
@@ -293,7 +296,8 @@ def run_ours(args, cfg):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**workload(cfg), "parallelism": f"dp{world} (point shards, NCCL allreduce)",
                        "nnz_upper": info["nnz_upper"], "n_tiles": info["n_tiles"],
-                       "setup_ms": info["setup_ms"], "sum_k": sum_k, "sum_k2": sum_k2},
+                       "setup_ms": info["setup_ms"], "sum_k": sum_k, "sum_k2": sum_k2,
+                       "tile_edge": info["tile_edge"], "max_tile_centres": info["max_tile_centres"]},
             "clocks": clocks.summary(), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "fit": fit}
     print(json.dumps(line), flush=True)

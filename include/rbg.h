@@ -161,6 +161,11 @@ rbg_status rbg_support_counts(rbg_ctx* ctx, const double* points, uint64_t nq, u
                               uint64_t* sum_k2);
 /* fp64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flops), microbenchmark. */
 rbg_status rbg_fp64_peak(rbg_ctx* ctx, double* tflops);
+/* Correctly rounded sqrt used by the tiled kernel vs __dsqrt_rn on 2n inputs. */
+rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
+/* Tile edge = support radius / divisor (1..16; default 4) for the next
+ * rbg_set_centres -- a performance knob, results are unaffected. */
+rbg_status rbg_set_tile_divisor(rbg_ctx* ctx, double divisor);
 /* Device time of the last assembly: point binning and tiled numeric phase. */
 rbg_status rbg_assembly_times(rbg_ctx* ctx, double* bin_ms, double* tiles_ms);
 

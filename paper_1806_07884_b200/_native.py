@@ -99,6 +99,8 @@ _SIGS = {
     "rbg_support_counts": (C.c_int, [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64)]),
     "rbg_fp64_peak": (C.c_int, [_P, _D]),
     "rbg_assembly_times": (C.c_int, [_P, _D, _D]),
+    "rbg_sqrt_selftest": (C.c_int, [_P, _U64, _U64, C.POINTER(_U64)]),
+    "rbg_set_tile_divisor": (C.c_int, [_P, C.c_double]),
 }
 
 _lib = None

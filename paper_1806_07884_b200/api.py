@@ -101,6 +101,15 @@ class Engine:
         except Exception:
             pass
 
+    def set_tile_divisor(self, divisor: float) -> None:
+        """Tile edge = radius / divisor for the next set_centres (perf knob)."""
+        self._check(self._L.rbg_set_tile_divisor(self._ctx, float(divisor)))
+
+    def sqrt_selftest(self, n: int = 1 << 24, seed: int = 1) -> int:
+        bad = C.c_uint64()
+        self._check(self._L.rbg_sqrt_selftest(self._ctx, n, seed, C.byref(bad)))
+        return int(bad.value)
+
     def set_stream(self, stream: int | None) -> None:
         self._check(self._L.rbg_set_stream(self._ctx, stream))
 

@@ -44,6 +44,26 @@ __global__ void support_count_kernel(GridDev g, const uint64_t* __restrict__ cpt
     }
 }
 
+// sqrt_rn_nonneg vs __dsqrt_rn on n pseudo-random doubles spread over
+// [2^-60, 2^4) (exponent and mantissa uniform) plus exact squares.
+__global__ void sqrt_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long* bad) {
+    unsigned long long nbad = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = (i + 1) * 0x9e3779b97f4a7c15ull ^ seed;
+        k ^= k >> 31;
+        k *= 0xbf58476d1ce4e5b9ull;
+        k ^= k >> 29;
+        const uint64_t mant = k & 0xfffffffffffffull;
+        const uint64_t ex = 1023 - 60 + ((k >> 52) % 64);
+        const double x = __longlong_as_double((long long)((ex << 52) | mant));
+        if (sqrt_rn_nonneg(x) != __dsqrt_rn(x)) ++nbad;
+        const double sq = (double)(i & 0xffffff) * (double)(i & 0xffffff);
+        if (sqrt_rn_nonneg(sq) != __dsqrt_rn(sq)) ++nbad;
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
 constexpr int kChains = 8;
 constexpr int kIters = 2048;
 
@@ -142,4 +162,29 @@ extern "C" rbg_status rbg_assembly_times(rbg_ctx* ctx, double* bin_ms, double* t
         ctx->err = e.what();
         return e.code;
     }
+}
+
+extern "C" rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    if (!ctx || !mismatches) return RBG_INVALID_ARGUMENT;
+    try {
+        RBG_CUDA(cudaSetDevice(ctx->device));
+        ctx->counters.reserve(4);
+        RBG_CUDA(cudaMemsetAsync(ctx->counters.p + 3, 0, sizeof(unsigned long long), ctx->stream));
+        rbg::sqrt_selftest_kernel<<<148 * 16, 256, 0, ctx->stream>>>(n, seed, ctx->counters.p + 3);
+        RBG_CHECK_LAUNCH(ctx);
+        unsigned long long h = 0;
+        RBG_CUDA(cudaMemcpyAsync(&h, ctx->counters.p + 3, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        RBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        *mismatches = h;
+        return RBG_OK;
+    } catch (const rbg::Error& e) {
+        ctx->err = e.what();
+        return e.code;
+    }
+}
+
+extern "C" rbg_status rbg_set_tile_divisor(rbg_ctx* ctx, double divisor) {
+    if (!ctx || !(divisor >= 1.0 && divisor <= 16.0)) return RBG_INVALID_ARGUMENT;
+    ctx->tile_div = divisor;
+    return RBG_OK;
 }

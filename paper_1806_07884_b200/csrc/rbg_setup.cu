@@ -205,6 +205,51 @@ __global__ void tile_map_kernel(const uint64_t* __restrict__ cptr, uint64_t n_ti
     }
 }
 
+// One block per bucketed tile: pack its centres, row starts, ids and slot map.
+template <int DIM>
+__global__ void build_blobs_kernel(const uint32_t* __restrict__ tiles, uint64_t n, int lb,
+                                   const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ cids,
+                                   const uint64_t* __restrict__ mptr, const uint16_t* __restrict__ map,
+                                   const double* __restrict__ centres, const uint64_t* __restrict__ uptr,
+                                   unsigned char* __restrict__ blobs) {
+    const BlobLayout B = blob_layout(DIM, lb);
+    for (uint64_t it = blockIdx.x; it < n; it += gridDim.x) {
+        const uint32_t t = tiles[it];
+        unsigned char* blob = blobs + it * B.bytes;
+        const uint64_t c0 = cptr[t];
+        const uint32_t L = (uint32_t)(cptr[t + 1] - c0);
+        if (threadIdx.x == 0) {
+            reinterpret_cast<uint32_t*>(blob)[0] = L;
+            reinterpret_cast<uint32_t*>(blob)[1] = t;
+        }
+        double* cx = reinterpret_cast<double*>(blob + B.cx);
+        double* cy = reinterpret_cast<double*>(blob + B.cy);
+        double* cz = reinterpret_cast<double*>(blob + B.cz);
+        uint64_t* up = reinterpret_cast<uint64_t*>(blob + B.uptr);
+        uint32_t* id = reinterpret_cast<uint32_t*>(blob + B.cid);
+        for (int a = threadIdx.x; a < lb; a += blockDim.x) {
+            if (a < (int)L) {
+                const uint32_t g = cids[c0 + a];
+                cx[a] = centres[(uint64_t)g * DIM];
+                cy[a] = centres[(uint64_t)g * DIM + 1];
+                if (DIM == 3) cz[a] = centres[(uint64_t)g * DIM + 2];
+                up[a] = uptr[g];
+                id[a] = g;
+            } else {
+                cx[a] = 0.0;
+                cy[a] = 0.0;
+                if (DIM == 3) cz[a] = 0.0;
+                up[a] = 0;
+                id[a] = 0;
+            }
+        }
+        uint16_t* mp = reinterpret_cast<uint16_t*>(blob + B.map);
+        const uint64_t m0 = mptr[t];
+        const uint32_t nm = L * (L + 1) / 2;
+        for (uint32_t e = threadIdx.x; e < nm; e += blockDim.x) mp[e] = map[m0 + e];
+    }
+}
+
 }  // namespace
 
 void setup_centres(rbg_ctx* ctx) {
@@ -227,7 +272,7 @@ void setup_centres(rbg_ctx* ctx) {
     const double r = ctx->radius;
     TileGrid g;
     g.dim = dim;
-    double edge = r / 4.0;
+    double edge = r / (ctx->tile_div > 0.0 ? ctx->tile_div : (dim == 2 ? 4.0 : 4.0));
     for (;;) {
         uint64_t total = 1;
         bool over = false;
@@ -424,6 +469,25 @@ void setup_centres(rbg_ctx* ctx) {
             ctx->ucols.p, ctx->tile_map.p);
         RBG_CHECK_LAUNCH(ctx);
     }
+
+    // ---- per-tile blobs for the persistent TMA-fed kernels ---------------------
+    for (Bucket& bk : ctx->buckets) {
+        if (bk.n_tiles == 0) continue;
+        const BlobLayout B = blob_layout(dim, bk.lb);
+        bk.blobs.reserve(bk.n_tiles * B.bytes);
+        bk.grid = 0;
+        const unsigned g = (unsigned)std::min<uint64_t>(bk.n_tiles, 148u * 32u);
+        if (dim == 2)
+            build_blobs_kernel<2><<<g, 128, 0, st>>>(bk.tiles.p, bk.n_tiles, bk.lb, ctx->tile_cptr.p,
+                                                     ctx->tile_cids.p, ctx->tile_mptr.p, ctx->tile_map.p,
+                                                     ctx->centres.p, ctx->uptr.p, bk.blobs.p);
+        else
+            build_blobs_kernel<3><<<g, 128, 0, st>>>(bk.tiles.p, bk.n_tiles, bk.lb, ctx->tile_cptr.p,
+                                                     ctx->tile_cids.p, ctx->tile_mptr.p, ctx->tile_map.p,
+                                                     ctx->centres.p, ctx->uptr.p, bk.blobs.p);
+        RBG_CHECK_LAUNCH(ctx);
+    }
+    ctx->work.reserve(ctx->buckets.size() + 1);
 
     // ---- system + point workspace sized for this centre set ----------------
     ctx->sys.reserve(ctx->nnz_upper + 2 * m);

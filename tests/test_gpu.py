@@ -210,3 +210,20 @@ def test_cfg2_full_size_properties(eng):
     c, diag = eng.solve()
     assert np.max(np.abs(c - c_true)) / np.max(np.abs(c_true)) < 1e-7
     del B
+
+
+def test_branchfree_sqrt_is_correctly_rounded(eng):
+    # the tiled kernel's sqrt must be bitwise __dsqrt_rn (A entries bitwise)
+    assert eng.sqrt_selftest(1 << 26, 12345) == 0
+
+
+@pytest.mark.parametrize("div", [2.0, 3.0, 5.0, 6.0])
+def test_tile_divisor_does_not_change_results(eng, div):
+    cfg = configs.CONFIGS["cfg1"]
+    xy, h = configs.points("cfg1", n=30_000)
+    refs = configs.centres("cfg1")
+    eng.set_tile_divisor(div)
+    try:
+        run_and_compare(eng, xy, h, refs, 1, cfg.alpha)
+    finally:
+        eng.set_tile_divisor(4.0)
