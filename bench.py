@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--tile-div", type=float, default=None, help="tile edge = radius / this")
+    ap.add_argument("--tile-div", type=float, default=None, help="sub-tile edge = radius / this")
+    ap.add_argument("--super-factor", type=int, default=None, help="super-tile = this^dim sub-tiles")
     return ap.parse_args()
 
 
@@ -215,6 +216,8 @@ def run_ours(args, cfg):
     eng = api.Engine(local, stream=stream.cuda_stream)
     if args.tile_div:
         eng.set_tile_divisor(args.tile_div)
+    if args.super_factor:
+        eng.set_super_factor(args.super_factor)
     eng.set_centres(refs, kernel)
     info = eng.pattern_info()
     d_xy = torch.from_numpy(xy).cuda()
@@ -232,6 +235,7 @@ def run_ours(args, cfg):
         step()
     torch.cuda.synchronize()
 
+    lay = eng.layout_info()
     # algorithmic work of one step on this rank (outside timing)
     sum_k, sum_k2 = _ncounts(eng, xy)
     flops_step = sum_k2 + (F_PHI[cfg.dim] + 3) * sum_k  # sum k F + k(k+1) + 2k
@@ -282,7 +286,7 @@ def run_ours(args, cfg):
         achieved = flops_step / t_tile / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": _traffic(cfg.name),
-                "kernel": "assemble_tiles_kernel (all buckets; tiled SYRK + slot-map flush)",
+                "kernel": "assemble_super_kernel (all buckets; sub-tile DMMA SYRK + super-tile smem accumulator + slot-map flush)",
                 "peak_source": "measured live: rbg_fp64_peak DFMA microbenchmark (MEASURED_PEAKS.json has no fp64)",
                 "algorithmic_flops_per_launch": flops_step, "tile_ms": t_tile * 1e3,
                 "bin_ms": statistics.median(bin_ms),
@@ -297,7 +301,13 @@ def run_ours(args, cfg):
             "config": {**workload(cfg), "parallelism": f"dp{world} (point shards, NCCL allreduce)",
                        "nnz_upper": info["nnz_upper"], "n_tiles": info["n_tiles"],
                        "setup_ms": info["setup_ms"], "sum_k": sum_k, "sum_k2": sum_k2,
-                       "tile_edge": info["tile_edge"], "max_tile_centres": info["max_tile_centres"]},
+                       "layout": {"sub_div": lay["sub_div"], "super_factor": lay["super_factor"],
+                                  "n_super": lay["n_super"], "n_buckets": lay["n_buckets"],
+                                  "n_fallback": lay["n_fallback"],
+                                  "mean_super_centres": round(lay["mean_super_centres"], 2),
+                                  "mean_sub_centres": round(lay["mean_sub_centres"], 2),
+                                  "max_super_centres": lay["max_super_centres"],
+                                  "max_sub_centres": lay["max_sub_centres"], "build_ms": round(lay["build_ms"], 2)}},
             "clocks": clocks.summary(), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "fit": fit}
     print(json.dumps(line), flush=True)

@@ -60,8 +60,9 @@ uint64_t rbg_launch_count(const rbg_ctx* ctx);
  * (solver.hpp:61-69, solver.cpp:151-156).  centres: m points, AoS, `dim`
  * (2 or 3) doubles each.  Validation as KernelSpec (kernel.cpp:35-38) and
  * assemble_submatrix (coo.cpp:168-175).  Builds the uniform tile grid, the
- * per-tile centre lists, the upper CSR pattern {(i,j): i<=j,
- * |c_i-c_j|^2 < (2/alpha)^2} and the per-tile slot maps. */
+ * per-tile centre lists (evaluation) and the upper CSR pattern {(i,j): i<=j,
+ * |c_i-c_j|^2 < (2/alpha)^2}; the assembly layout (super/sub-tiles, slot
+ * maps) follows at the first assembly. */
 rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_t m,
                            int kernel_family, double alpha);
 
@@ -70,7 +71,7 @@ typedef struct {
     uint64_t nnz_upper;    /* pattern entries, upper triangle incl. diagonal */
     uint64_t nnz_full;     /* symmetric pattern entries */
     uint64_t n_tiles;      /* tile grid size */
-    uint64_t n_fallback;   /* tiles whose centre list exceeds the tiled kernel */
+    uint64_t n_fallback;   /* super-tiles on the slow path (0 before the first assembly) */
     uint32_t max_tile_centres;
     double tile_edge;
     double setup_ms;       /* device time of rbg_set_centres */
@@ -163,9 +164,26 @@ rbg_status rbg_support_counts(rbg_ctx* ctx, const double* points, uint64_t nq, u
 rbg_status rbg_fp64_peak(rbg_ctx* ctx, double* tflops);
 /* Correctly rounded sqrt used by the tiled kernel vs __dsqrt_rn on 2n inputs. */
 rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
-/* Tile edge = support radius / divisor (1..16; default 4) for the next
- * rbg_set_centres -- a performance knob, results are unaffected. */
+/* Assembly layout knobs (performance only; results are unaffected beyond
+ * fp64 summation order): sub-tile edge = support radius / divisor (1..16,
+ * 0 = automatic from the point density) and super-tile = S x S (x S)
+ * sub-tiles (1..8, 0 = automatic).  The layout is rebuilt at the next
+ * assembly. */
 rbg_status rbg_set_tile_divisor(rbg_ctx* ctx, double divisor);
+rbg_status rbg_set_super_factor(rbg_ctx* ctx, int S);
+typedef struct {
+    int built;             /* 0 until the first assembly after rbg_set_centres */
+    int sub_div;           /* q: sub-tile edge = radius / q (before growth for huge grids) */
+    int super_factor;      /* S */
+    int n_buckets;         /* launch classes */
+    uint64_t n_super;      /* super-tiles */
+    uint64_t n_fallback;   /* super-tiles on the slow per-point path */
+    uint32_t max_super_centres, max_sub_centres;
+    double mean_super_centres, mean_sub_centres;
+    double sub_edge;
+    double build_ms;       /* host wall time of the layout build */
+} rbg_layout_info;
+rbg_status rbg_get_layout_info(rbg_ctx* ctx, rbg_layout_info* info);
 /* Device time of the last assembly: point binning and tiled numeric phase. */
 rbg_status rbg_assembly_times(rbg_ctx* ctx, double* bin_ms, double* tiles_ms);
 

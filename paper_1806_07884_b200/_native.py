@@ -57,6 +57,14 @@ class PatternInfo(C.Structure):
                 ("setup_ms", C.c_double)]
 
 
+class LayoutInfo(C.Structure):
+    _fields_ = [("built", C.c_int), ("sub_div", C.c_int), ("super_factor", C.c_int), ("n_buckets", C.c_int),
+                ("n_super", C.c_uint64), ("n_fallback", C.c_uint64),
+                ("max_super_centres", C.c_uint32), ("max_sub_centres", C.c_uint32),
+                ("mean_super_centres", C.c_double), ("mean_sub_centres", C.c_double),
+                ("sub_edge", C.c_double), ("build_ms", C.c_double)]
+
+
 class SolveOptions(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int)]
 
@@ -101,6 +109,8 @@ _SIGS = {
     "rbg_assembly_times": (C.c_int, [_P, _D, _D]),
     "rbg_sqrt_selftest": (C.c_int, [_P, _U64, _U64, C.POINTER(_U64)]),
     "rbg_set_tile_divisor": (C.c_int, [_P, C.c_double]),
+    "rbg_set_super_factor": (C.c_int, [_P, C.c_int]),
+    "rbg_get_layout_info": (C.c_int, [_P, C.POINTER(LayoutInfo)]),
 }
 
 _lib = None

@@ -102,8 +102,18 @@ class Engine:
             pass
 
     def set_tile_divisor(self, divisor: float) -> None:
-        """Tile edge = radius / divisor for the next set_centres (perf knob)."""
+        """Assembly sub-tile edge = radius / divisor (0 = automatic; perf knob)."""
         self._check(self._L.rbg_set_tile_divisor(self._ctx, float(divisor)))
+
+    def set_super_factor(self, s: int) -> None:
+        """Super-tile = s^dim sub-tiles (0 = automatic; perf knob)."""
+        self._check(self._L.rbg_set_super_factor(self._ctx, int(s)))
+
+    def layout_info(self) -> dict:
+        """Assembly layout of the current centre set (built at the first assembly)."""
+        info = _native.LayoutInfo()
+        self._check(self._L.rbg_get_layout_info(self._ctx, C.byref(info)))
+        return {k: getattr(info, k) for k, _ in info._fields_}
 
     def sqrt_selftest(self, n: int = 1 << 24, seed: int = 1) -> int:
         bad = C.c_uint64()

@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
                      f"-I{ROOT / 'include'}"]
-CU_SOURCES = ["rbg_util.cu", "rbg_setup.cu", "rbg_assemble.cu", "rbg_solve.cu",
+CU_SOURCES = ["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu", "rbg_solve.cu",
               "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu"]
 
 LIB_RBG = PKG / "librbg.so"

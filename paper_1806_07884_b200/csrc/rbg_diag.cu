@@ -184,7 +184,33 @@ extern "C" rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed,
 }
 
 extern "C" rbg_status rbg_set_tile_divisor(rbg_ctx* ctx, double divisor) {
-    if (!ctx || !(divisor >= 1.0 && divisor <= 16.0)) return RBG_INVALID_ARGUMENT;
-    ctx->tile_div = divisor;
+    if (!ctx || !(divisor == 0.0 || (divisor >= 1.0 && divisor <= 16.0))) return RBG_INVALID_ARGUMENT;
+    ctx->sub_div_req = (int)(divisor + 0.5);
+    ctx->lay.built = false;
+    return RBG_OK;
+}
+
+extern "C" rbg_status rbg_set_super_factor(rbg_ctx* ctx, int S) {
+    if (!ctx || S < 0 || S > 8) return RBG_INVALID_ARGUMENT;
+    ctx->super_req = S;
+    ctx->lay.built = false;
+    return RBG_OK;
+}
+
+extern "C" rbg_status rbg_get_layout_info(rbg_ctx* ctx, rbg_layout_info* info) {
+    if (!ctx || !info) return RBG_INVALID_ARGUMENT;
+    const rbg::AsmLayout& L = ctx->lay;
+    info->built = L.built ? 1 : 0;
+    info->sub_div = L.q;
+    info->super_factor = L.S;
+    info->n_buckets = (int)L.buckets.size();
+    info->n_super = L.n_super;
+    info->n_fallback = L.n_fallback;
+    info->max_super_centres = L.max_ls;
+    info->max_sub_centres = L.max_lsub;
+    info->mean_super_centres = L.mean_ls;
+    info->mean_sub_centres = L.mean_lsub;
+    info->sub_edge = L.sub_edge;
+    info->build_ms = L.build_ms;
     return RBG_OK;
 }

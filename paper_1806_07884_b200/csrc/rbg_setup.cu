@@ -10,9 +10,9 @@
 //     dist2(c_i, c_j) < (2/alpha)^2 (the predicate every co-supported pair
 //     satisfies), columns ascending; plus the symmetric full pattern and the
 //     full->upper slot map the solver uses;
-//   * per tile, the packed upper-triangle slot map local (a,b) -> offset of
-//     column c_b within upper row c_a, so the numeric kernel flushes its
-//     register tiles without searching.
+//   * slot maps (tile_map_kernel): per tile list, the packed upper-triangle
+//     map local (a,b) -> offset of column c_b within upper row c_a, so the
+//     numeric kernel flushes without searching (used by rbg_layout.cu).
 #include <algorithm>
 #include <cmath>
 #include <numeric>
@@ -205,52 +205,48 @@ __global__ void tile_map_kernel(const uint64_t* __restrict__ cptr, uint64_t n_ti
     }
 }
 
-// One block per bucketed tile: pack its centres, row starts, ids and slot map.
-template <int DIM>
-__global__ void build_blobs_kernel(const uint32_t* __restrict__ tiles, uint64_t n, int lb,
-                                   const uint64_t* __restrict__ cptr, const uint32_t* __restrict__ cids,
-                                   const uint64_t* __restrict__ mptr, const uint16_t* __restrict__ map,
-                                   const double* __restrict__ centres, const uint64_t* __restrict__ uptr,
-                                   unsigned char* __restrict__ blobs) {
-    const BlobLayout B = blob_layout(DIM, lb);
-    for (uint64_t it = blockIdx.x; it < n; it += gridDim.x) {
-        const uint32_t t = tiles[it];
-        unsigned char* blob = blobs + it * B.bytes;
-        const uint64_t c0 = cptr[t];
-        const uint32_t L = (uint32_t)(cptr[t + 1] - c0);
-        if (threadIdx.x == 0) {
-            reinterpret_cast<uint32_t*>(blob)[0] = L;
-            reinterpret_cast<uint32_t*>(blob)[1] = t;
-        }
-        double* cx = reinterpret_cast<double*>(blob + B.cx);
-        double* cy = reinterpret_cast<double*>(blob + B.cy);
-        double* cz = reinterpret_cast<double*>(blob + B.cz);
-        uint64_t* up = reinterpret_cast<uint64_t*>(blob + B.uptr);
-        uint32_t* id = reinterpret_cast<uint32_t*>(blob + B.cid);
-        for (int a = threadIdx.x; a < lb; a += blockDim.x) {
-            if (a < (int)L) {
-                const uint32_t g = cids[c0 + a];
-                cx[a] = centres[(uint64_t)g * DIM];
-                cy[a] = centres[(uint64_t)g * DIM + 1];
-                if (DIM == 3) cz[a] = centres[(uint64_t)g * DIM + 2];
-                up[a] = uptr[g];
-                id[a] = g;
-            } else {
-                cx[a] = 0.0;
-                cy[a] = 0.0;
-                if (DIM == 3) cz[a] = 0.0;
-                up[a] = 0;
-                id[a] = 0;
-            }
-        }
-        uint16_t* mp = reinterpret_cast<uint16_t*>(blob + B.map);
-        const uint64_t m0 = mptr[t];
-        const uint32_t nm = L * (L + 1) / 2;
-        for (uint32_t e = threadIdx.x; e < nm; e += blockDim.x) mp[e] = map[m0 + e];
-    }
+}  // namespace
+
+// Centre lists of every tile of grid g (ascending ids): count, scan, fill, sort.
+void tile_lists(rbg_ctx* ctx, const TileGrid& g, DevBuf<uint32_t>& count, DevBuf<uint64_t>& cptr,
+                DevBuf<uint32_t>& cids, std::vector<uint64_t>& host_cptr) {
+    cudaStream_t st = ctx->stream;
+    const uint64_t nt = g.count, m = ctx->m;
+    count.reserve(nt + 1);
+    cptr.reserve(nt + 1);
+    RBG_CUDA(cudaMemsetAsync(count.p, 0, (nt + 1) * sizeof(uint32_t), st));
+    TileTestDev tt{grid_dev(g), g.edge, g.edge * kTileMargin, ctx->radius, ctx->r2 * (1.0 + 1e-6)};
+    const unsigned cb = blocks_for(m, 128);
+    if (g.dim == 2)
+        tile_lists_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, count.p, nullptr, nullptr);
+    else
+        tile_lists_kernel<3, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, count.p, nullptr, nullptr);
+    RBG_CHECK_LAUNCH(ctx);
+    exclusive_scan_u32_to_u64(ctx, count.p, cptr.p, nt);
+    host_cptr.assign(nt + 1, 0);
+    RBG_CUDA(cudaMemcpyAsync(host_cptr.data(), cptr.p, (nt + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    const uint64_t total = host_cptr[nt];
+    cids.reserve(std::max<uint64_t>(total, 1));
+    RBG_CUDA(cudaMemsetAsync(count.p, 0, (nt + 1) * sizeof(uint32_t), st));
+    if (g.dim == 2)
+        tile_lists_kernel<2, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, count.p, cptr.p, cids.p);
+    else
+        tile_lists_kernel<3, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, count.p, cptr.p, cids.p);
+    RBG_CHECK_LAUNCH(ctx);
+    uint32_t max_l = 0;
+    for (uint64_t t = 0; t < nt; ++t) max_l = std::max<uint32_t>(max_l, (uint32_t)(host_cptr[t + 1] - host_cptr[t]));
+    segmented_sort_u32(ctx, cids.p, cptr.p, nt, max_l);
 }
 
-}  // namespace
+// Packed upper-triangle slot maps of every tile's centre list (needs the pattern).
+void slot_maps(rbg_ctx* ctx, const uint64_t* cptr, uint64_t n_tiles, const uint32_t* cids, uint64_t total_ids,
+               const uint64_t* mptr, uint16_t* map) {
+    if (total_ids == 0) return;
+    tile_map_kernel<<<blocks_for(total_ids, 256), 256, 0, ctx->stream>>>(cptr, n_tiles, cids, total_ids, mptr,
+                                                                          ctx->uptr.p, ctx->ucols.p, map);
+    RBG_CHECK_LAUNCH(ctx);
+}
 
 void setup_centres(rbg_ctx* ctx) {
     const int dim = ctx->dim;
@@ -272,7 +268,7 @@ void setup_centres(rbg_ctx* ctx) {
     const double r = ctx->radius;
     TileGrid g;
     g.dim = dim;
-    double edge = r / (ctx->tile_div > 0.0 ? ctx->tile_div : (dim == 2 ? 4.0 : 4.0));
+    double edge = r / 4.0;
     for (;;) {
         uint64_t total = 1;
         bool over = false;
@@ -301,74 +297,13 @@ void setup_centres(rbg_ctx* ctx) {
     ctx->grid = g;
     const uint64_t nt = g.count;
 
-    // ---- K1: tile centre lists ---------------------------------------------
-    ctx->tile_count.reserve(nt + 1);
-    ctx->tile_cptr.reserve(nt + 1);
-    RBG_CUDA(cudaMemsetAsync(ctx->tile_count.p, 0, (nt + 1) * sizeof(uint32_t), st));
-    TileTestDev tt{grid_dev(g), edge, edge * kTileMargin, r, ctx->r2 * (1.0 + 1e-6)};
-    const unsigned cb = blocks_for(m, 128);
-    if (dim == 2)
-        tile_lists_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
-                                                        nullptr, nullptr);
-    else
-        tile_lists_kernel<3, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
-                                                        nullptr, nullptr);
-    RBG_CHECK_LAUNCH(ctx);
-    exclusive_scan_u32_to_u64(ctx, ctx->tile_count.p, ctx->tile_cptr.p, nt);
-    std::vector<uint64_t> cptr(nt + 1);
-    RBG_CUDA(cudaMemcpyAsync(cptr.data(), ctx->tile_cptr.p, (nt + 1) * sizeof(uint64_t),
-                             cudaMemcpyDeviceToHost, st));
-    RBG_CUDA(cudaStreamSynchronize(st));
-    const uint64_t total_ids = cptr[nt];
-    ctx->tile_cids.reserve(std::max<uint64_t>(total_ids, 1));
-    RBG_CUDA(cudaMemsetAsync(ctx->tile_count.p, 0, (nt + 1) * sizeof(uint32_t), st));
-    if (dim == 2)
-        tile_lists_kernel<2, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
-                                                       ctx->tile_cptr.p, ctx->tile_cids.p);
-    else
-        tile_lists_kernel<3, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, tt, ctx->tile_count.p,
-                                                       ctx->tile_cptr.p, ctx->tile_cids.p);
-    RBG_CHECK_LAUNCH(ctx);
+    // ---- K1: query-tile centre lists (evaluation / support counts) ----------
+    std::vector<uint64_t> cptr;
+    tile_lists(ctx, g, ctx->tile_count, ctx->tile_cptr, ctx->tile_cids, cptr);
     uint32_t max_l = 0;
     for (uint64_t t = 0; t < nt; ++t) max_l = std::max<uint32_t>(max_l, (uint32_t)(cptr[t + 1] - cptr[t]));
     ctx->max_tile_centres = max_l;
-    segmented_sort_u32(ctx, ctx->tile_cids.p, ctx->tile_cptr.p, nt, max_l);
-
-    // ---- buckets + slot-map offsets (host) ----------------------------------
-    static const int kBuckets[] = {16, 24, 32, 40, 48, 56, 64, 72, 80, 96, 112, 128, 160};
-    std::vector<std::vector<uint32_t>> lists(std::size(kBuckets));
-    std::vector<uint32_t> fallback;
-    std::vector<uint64_t> mptr(nt + 1, 0);
-    for (uint64_t t = 0; t < nt; ++t) {
-        const uint64_t L = cptr[t + 1] - cptr[t];
-        mptr[t + 1] = mptr[t] + L * (L + 1) / 2;
-        if (L == 0) continue;
-        size_t b = 0;
-        while (b < std::size(kBuckets) && (uint64_t)kBuckets[b] < L) ++b;
-        if (b == std::size(kBuckets)) fallback.push_back((uint32_t)t);
-        else lists[b].push_back((uint32_t)t);
-    }
-    ctx->buckets.clear();
-    ctx->buckets.resize(std::size(kBuckets));
-    for (size_t b = 0; b < std::size(kBuckets); ++b) {
-        Bucket& bk = ctx->buckets[b];
-        bk.lb = kBuckets[b];
-        bk.n_tiles = lists[b].size();
-        if (bk.n_tiles) {
-            bk.tiles.reserve(bk.n_tiles);
-            RBG_CUDA(cudaMemcpyAsync(bk.tiles.p, lists[b].data(), bk.n_tiles * sizeof(uint32_t),
-                                     cudaMemcpyHostToDevice, st));
-        }
-    }
-    ctx->n_fallback = fallback.size();
-    if (!fallback.empty()) {
-        ctx->fallback_tiles.reserve(fallback.size());
-        RBG_CUDA(cudaMemcpyAsync(ctx->fallback_tiles.p, fallback.data(),
-                                 fallback.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    }
-    ctx->tile_mptr.reserve(nt + 1);
-    RBG_CUDA(cudaMemcpyAsync(ctx->tile_mptr.p, mptr.data(), (nt + 1) * sizeof(uint64_t),
-                             cudaMemcpyHostToDevice, st));
+    const unsigned cb = blocks_for(m, 128);
 
     // ---- K2: pattern --------------------------------------------------------
     const double two_r = 2.0 * r;
@@ -461,37 +396,10 @@ void setup_centres(rbg_ctx* ctx) {
                                              ctx->ucols.p, ctx->f2u.p);
     RBG_CHECK_LAUNCH(ctx);
 
-    // ---- per-tile slot maps -------------------------------------------------
-    ctx->tile_map.reserve(std::max<uint64_t>(mptr[nt], 1));
-    if (total_ids > 0) {
-        tile_map_kernel<<<blocks_for(total_ids, 256), 256, 0, st>>>(
-            ctx->tile_cptr.p, nt, ctx->tile_cids.p, total_ids, ctx->tile_mptr.p, ctx->uptr.p,
-            ctx->ucols.p, ctx->tile_map.p);
-        RBG_CHECK_LAUNCH(ctx);
-    }
-
-    // ---- per-tile blobs for the persistent TMA-fed kernels ---------------------
-    for (Bucket& bk : ctx->buckets) {
-        if (bk.n_tiles == 0) continue;
-        const BlobLayout B = blob_layout(dim, bk.lb);
-        bk.blobs.reserve(bk.n_tiles * B.bytes);
-        bk.grid = 0;
-        const unsigned g = (unsigned)std::min<uint64_t>(bk.n_tiles, 148u * 32u);
-        if (dim == 2)
-            build_blobs_kernel<2><<<g, 128, 0, st>>>(bk.tiles.p, bk.n_tiles, bk.lb, ctx->tile_cptr.p,
-                                                     ctx->tile_cids.p, ctx->tile_mptr.p, ctx->tile_map.p,
-                                                     ctx->centres.p, ctx->uptr.p, bk.blobs.p);
-        else
-            build_blobs_kernel<3><<<g, 128, 0, st>>>(bk.tiles.p, bk.n_tiles, bk.lb, ctx->tile_cptr.p,
-                                                     ctx->tile_cids.p, ctx->tile_mptr.p, ctx->tile_map.p,
-                                                     ctx->centres.p, ctx->uptr.p, bk.blobs.p);
-        RBG_CHECK_LAUNCH(ctx);
-    }
-    ctx->work.reserve(ctx->buckets.size() + 1);
+    ctx->lay = AsmLayout();  // rebuilt at the next assembly for this centre set
 
     // ---- system + point workspace sized for this centre set ----------------
     ctx->sys.reserve(ctx->nnz_upper + 2 * m);
-    ctx->tile_pptr.reserve(nt + 1);
     ctx->counters.reserve(4);
     RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
     RBG_CUDA(cudaStreamSynchronize(st));

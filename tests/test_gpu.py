@@ -114,14 +114,14 @@ def test_slab_accumulation_equals_single(eng):
 
 
 def test_fallback_tiles_dense_centres(eng):
-    # centre lists above the largest register tile (160) take the slow path
+    # super-tile centre lists above the largest accumulator class take the slow path
     rng = np.random.default_rng(11)
     refs = rng.random((400, 2)) * 0.2
     pts = rng.random((3000, 2)) * 0.3
     h = rng.standard_normal(3000)
     eng.set_centres(refs, api.KernelSpec("wendland-3-1", 8.0))
-    assert eng.pattern_info()["n_fallback"] > 0
     run_and_compare(eng, pts, h, refs, 1, 8.0)
+    assert eng.layout_info()["n_fallback"] > 0
 
 
 @pytest.mark.parametrize("family", [0, 1, 2, 3])
@@ -217,13 +217,18 @@ def test_branchfree_sqrt_is_correctly_rounded(eng):
     assert eng.sqrt_selftest(1 << 26, 12345) == 0
 
 
-@pytest.mark.parametrize("div", [2.0, 3.0, 5.0, 6.0])
-def test_tile_divisor_does_not_change_results(eng, div):
+@pytest.mark.parametrize("div,sup", [(2.0, 1), (3.0, 2), (5.0, 3), (6.0, 4), (8.0, 2), (12.0, 5)])
+def test_layout_does_not_change_results(eng, div, sup):
+    # sub-tile divisor / super-tile factor are performance knobs only
     cfg = configs.CONFIGS["cfg1"]
     xy, h = configs.points("cfg1", n=30_000)
     refs = configs.centres("cfg1")
     eng.set_tile_divisor(div)
+    eng.set_super_factor(sup)
     try:
         run_and_compare(eng, xy, h, refs, 1, cfg.alpha)
+        info = eng.layout_info()
+        assert info["built"] and info["sub_div"] == int(div) and info["super_factor"] == sup
     finally:
-        eng.set_tile_divisor(4.0)
+        eng.set_tile_divisor(0)
+        eng.set_super_factor(0)
