@@ -107,5 +107,7 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
+    if "--check" in sys.argv:  # device bounds checks (debugging only)
+        NVCC_FLAGS.append("-DRBG_DEVCHECK")
+    build_all(force="--force" in sys.argv or "--check" in sys.argv)
     print("built:", LIB_RBG, LIB_HOST, LIB_DATAGEN)

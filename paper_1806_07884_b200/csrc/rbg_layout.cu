@@ -154,8 +154,8 @@ __global__ void build_blobs_kernel(const uint32_t* __restrict__ items, uint64_t 
     }
 }
 
-// SYRK register classes (fixes the per-warp 8x8 block count, see rbg_assemble.cu)
-constexpr int kSubCaps[] = {32, 48, 64, 80, 104, 128};
+// sub-tile list capacities (gather rows per warp, see rbg_assemble.cu)
+constexpr int kSubCaps[] = {32, 56, 64, 80, 120, 160, 200, 240};
 // accumulator classes (shared-memory upper triangle of L_S x L_S)
 constexpr int kSuperCaps[] = {32, 48, 64, 80, 96, 112, 128, 160, 192};
 
@@ -362,7 +362,7 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     }
     ctx->work.reserve(L.buckets.size() + 1);
     ctx->tile_count.reserve(L.n_keys + 1);
-    ctx->tile_pptr.reserve(L.n_keys + 3);
+    ctx->tile_pptr.reserve(L.n_keys + 1);
     RBG_CUDA(cudaStreamSynchronize(st));
     L.built = true;
     L.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
