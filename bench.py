@@ -286,7 +286,7 @@ def run_ours(args, cfg):
         achieved = flops_step / t_tile / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": _traffic(cfg.name),
-                "kernel": "assemble_super_kernel (all buckets; sub-tile DMMA SYRK + super-tile smem accumulator + slot-map flush)",
+                "kernel": "assemble_warp_kernel (persistent one-warp workers: phi into DMMA fragments, register SYRK per sub-tile, warp-private super-tile accumulator, slot-map flush)",
                 "peak_source": "measured live: rbg_fp64_peak DFMA microbenchmark (MEASURED_PEAKS.json has no fp64)",
                 "algorithmic_flops_per_launch": flops_step, "tile_ms": t_tile * 1e3,
                 "bin_ms": statistics.median(bin_ms),

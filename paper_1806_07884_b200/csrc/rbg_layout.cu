@@ -155,9 +155,9 @@ __global__ void build_blobs_kernel(const uint32_t* __restrict__ items, uint64_t 
 }
 
 // sub-tile list capacities (gather rows per warp, see rbg_assemble.cu)
-constexpr int kSubCaps[] = {32, 56, 64, 80, 120, 160, 200, 240};
+constexpr int kSubCaps[] = {32, 48, 56, 64, 80, 120, 160, 200, 240};
 // accumulator classes (shared-memory upper triangle of L_S x L_S)
-constexpr int kSuperCaps[] = {32, 48, 64, 80, 96, 112, 128, 160, 192};
+constexpr int kSuperCaps[] = {32, 40, 48, 56, 64, 72, 80, 88, 96, 112, 128, 160, 192};
 
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
@@ -167,23 +167,27 @@ int env_int(const char* name, int dflt) {
 }  // namespace
 
 // Sub-tile divisor q (sub edge = r/q) and super factor S from the point
-// density: about 32 points per sub-tile (one 32-point chunk of the SYRK),
-// super-tiles of about half a support radius.
+// density (measured on B200, profiles/): 2-D sub-tiles of about 34 points
+// (about nine 4-point DMMA k-steps per register pass), super-tiles of 2x2
+// sub-tiles, 3x3 once the sub-tiles are small (q >= 9); 3-D: sub-tiles of
+// edge r/2 assembled in direct mode (one sub-tile per super-tile, register
+// tiles reduced straight into the CSR values: a 3-D super-tile accumulator
+// would not fit shared memory).
 static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* span, int& q, int& S) {
     const int dim = ctx->dim;
     const double r = ctx->radius;
     double vol = 1.0;
     for (int d = 0; d < dim; ++d) vol *= std::max(span[d], r * 1e-3);
     const double rho = std::max(1.0, (double)n_points) / vol;
-    const double target = dim == 2 ? 24.0 : 20.0;
-    const double e = std::pow(target / rho, 1.0 / dim);
-    q = (int)std::lround(r / e);
-    q = std::max(dim == 2 ? 2 : 2, std::min(q, 16));
+    if (dim == 2) {
+        const double e = std::sqrt(34.0 / rho);
+        q = std::max(2, std::min(16, (int)std::lround(r / e)));
+        S = q >= 9 ? 3 : 2;
+    } else {
+        q = 2;
+        S = 1;
+    }
     if (ctx->sub_div_req > 0) q = ctx->sub_div_req;
-    // super edge ~ r/2 (2-D) or r/2 (3-D), at least one sub-tile
-    S = std::max(1, (int)std::lround(q / 2.0));
-    if (dim == 2) S = std::min(S, 4);
-    else S = std::min(S, 2);
     if (ctx->super_req > 0) S = ctx->super_req;
     const int qe = env_int("RBG_SUB_DIV", 0), se = env_int("RBG_SUPER", 0);
     if (qe > 0) q = qe;
