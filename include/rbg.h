@@ -130,9 +130,10 @@ rbg_status rbg_solve(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out,
 
 /* ---- evaluation -------------------------------------------------------------
  * Replaces evaluate_model / evaluate_shifted (model.cpp:50-72,192-194) with a
- * zero offset and no polynomial: f_q = sum_j c_j phi(|q - xi_j|) over the
+ * zero offset: f_q = sum_j c_j phi(|q - xi_j|) over the
  * support hits in ascending j, unfused mul/add -- bitwise equal to the
- * reference for the same c.  c: m doubles; q: nq points (AoS). */
+ * reference for the same c, plus the polynomial term when one is set
+ * (rbg_set_model_poly).  c: m doubles; q: nq points (AoS). */
 rbg_status rbg_evaluate(rbg_ctx* ctx, const double* c, const double* q, uint64_t nq, double* f);
 rbg_status rbg_evaluate_device(rbg_ctx* ctx, const double* d_c, const double* d_q, uint64_t nq,
                                double* d_f);
@@ -148,6 +149,22 @@ typedef struct {
 } rbg_error_stats;
 rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points, const double* h,
                             uint64_t n, rbg_error_stats* out, double* signed_errors);
+
+/* ---- linear-polynomial border (FitOptions::poly, solver.hpp:113-118) ---------
+ * With the border enabled the system is the reference's bordered one
+ * (solver.cpp:189-207, 238-262): side = m + T with T = dim + 1 terms
+ * P = [x, y, (z), 1] per point; rbg_assemble then also accumulates
+ * A^T P (T x m, term-major), P^T P (T x T) and P^T h (T), appended to the
+ * device system buffer [values | rhs | hits | A^T P | P^T P | P^T h] (the unit
+ * of the multi-GPU all-reduce, rbg_system_device), and rbg_solve solves the
+ * bordered system; its border coefficients come from rbg_get_poly_solution
+ * (Weights::poly, solver.hpp:102-105).  rbg_set_model_poly makes evaluation
+ * add a_0 x + a_1 y (+ a_2 z) + a_T-1 (model.cpp:65-68); NULL removes it. */
+rbg_status rbg_set_poly(rbg_ctx* ctx, int enable);
+rbg_status rbg_get_border(rbg_ctx* ctx, double* atp, double* ptp, double* pth);
+rbg_status rbg_set_border(rbg_ctx* ctx, const double* atp, const double* ptp, const double* pth);
+rbg_status rbg_get_poly_solution(rbg_ctx* ctx, double* a);
+rbg_status rbg_set_model_poly(rbg_ctx* ctx, const double* a);
 
 /* ---- host-side helpers (no device work) ------------------------------------ */
 /* Spatial slabs for multi-GPU sharding: writes n_slabs+1 boundaries along

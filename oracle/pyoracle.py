@@ -53,6 +53,8 @@ def orc() -> C.CDLL:
                                          C.POINTER(C.c_int64)]
         L.orc_pcg.argtypes = [_U64, _P, _P, _P, _P, C.c_double, C.c_double, C.c_int, _P,
                               C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.orc_border.argtypes = [C.c_int, _P, _P, _U64, _P, _U64, C.c_int, C.c_double, _P, _P, _P]
+        L.orc_evaluate_poly.argtypes = [C.c_int, _P, _U64, _P, _P, C.c_int, C.c_double, _P, _U64, _P]
         L.orc_densify.argtypes = [_U64, _P, _P, _P, _P]
         L.orc_densify.restype = None
         _orc = L
@@ -86,6 +88,8 @@ def ref() -> C.CDLL:
         L.ref_error_report.argtypes = [_P, _P, _U64, C.c_int, C.c_double, _P, _P, _U64, _P, _P]
         L.ref_bench_step.argtypes = [_P, _P, _U64, _P, _U64, C.c_int, C.c_double, C.POINTER(C.c_double),
                                      C.POINTER(_U64)]
+        L.ref_border.argtypes = [_P, _P, _U64, _P, _U64, C.c_int, C.c_double, _P, _P, _P]
+        L.ref_evaluate_model_poly.argtypes = [_P, _P, _P, _U64, C.c_int, C.c_double, _P, _U64, _P]
         _ref = L
     return _ref
 
@@ -135,6 +139,36 @@ def evaluate(centres, w, family, alpha, queries):
     f = np.empty(q.shape[0])
     _ok(orc().orc_evaluate(c.shape[1], _p(c), c.shape[0], _p(ww), family, alpha, _p(q), q.shape[0], _p(f)))
     return f
+
+
+def border(points, values, centres, family, alpha):
+    """A^T P (T x m), P^T P, P^T h of the linear-polynomial border."""
+    p, h, c = _f64(points), _f64(values), _f64(centres)
+    n, dim = p.shape
+    m, T = c.shape[0], dim + 1
+    atp, ptp, pth = np.empty((T, m)), np.empty((T, T)), np.empty(T)
+    _ok(orc().orc_border(dim, _p(p), _p(h), n, _p(c), m, family, alpha, _p(atp), _p(ptp), _p(pth)))
+    return {"atp": atp, "ptp": ptp, "pth": pth}
+
+
+def evaluate_poly(centres, w, a, family, alpha, queries):
+    c, ww, aa, q = _f64(centres), _f64(w), _f64(a), _f64(queries)
+    f = np.empty(q.shape[0])
+    _ok(orc().orc_evaluate_poly(c.shape[1], _p(c), c.shape[0], _p(ww), _p(aa), family, alpha, _p(q),
+                                q.shape[0], _p(f)))
+    return f
+
+
+def bordered_dense(b, rhs, border):
+    """Dense bordered system [[B, A^T P], [P^T A, P^T P]] and [A^T h; P^T h]."""
+    atp, ptp, pth = border["atp"], border["ptp"], border["pth"]
+    m, T = b.shape[0], ptp.shape[0]
+    k = np.zeros((m + T, m + T))
+    k[:m, :m] = b
+    k[:m, m:] = atp.T
+    k[m:, :m] = atp
+    k[m:, m:] = ptp
+    return k, np.concatenate([rhs, pth])
 
 
 def error_report(f, h):
@@ -188,6 +222,25 @@ def ref_build_normal_system(points, values, refs, family, alpha, dense=True):
     _ok(st, L.ref_last_error().decode())
     return {"b": b, "rhs": rhs, "design_nnz": dn.value, "ref_nnz": ref_nnz,
             "times": {"index": times[0], "assembly": times[1], "gram": times[2]}}
+
+
+def ref_border(points, values, refs, family, alpha):
+    p, h, r = _f64(points), _f64(values), _f64(refs)
+    m = r.shape[0]
+    atp, ptp, pth = np.empty((3, m)), np.empty((3, 3)), np.empty(3)
+    L = ref()
+    _ok(L.ref_border(_p(p), _p(h), p.shape[0], _p(r), m, family, alpha, _p(atp), _p(ptp), _p(pth)),
+        L.ref_last_error().decode())
+    return {"atp": atp, "ptp": ptp, "pth": pth}
+
+
+def ref_evaluate_poly(refs, w, a, family, alpha, queries):
+    r, ww, aa, q = _f64(refs), _f64(w), _f64(a), _f64(queries)
+    f = np.empty(q.shape[0])
+    L = ref()
+    _ok(L.ref_evaluate_model_poly(_p(r), _p(ww), _p(aa), r.shape[0], family, alpha, _p(q), q.shape[0], _p(f)),
+        L.ref_last_error().decode())
+    return f
 
 
 def ref_evaluate(refs, w, family, alpha, queries):

@@ -535,3 +535,71 @@ void orc_densify(uint64_t m, const uint64_t* rp, const uint32_t* cols, const dou
             dense[(uint64_t)cols[e] * m + i] = vals[e];
         }
 }
+
+/* ------------------------------------------------ linear-polynomial border */
+
+/* The bordered system's extra blocks (solver.cpp:189-207, 238-262) with
+ * P = [x, y, (z), 1], T = dim + 1: atp[t*m + j] = sum_p A[p][j] * P[p][t]
+ * accumulated over the points in ascending order (the reference streams the
+ * triplets column by column, rows ascending), ptp = P^T P and pth = P^T h in
+ * one pass over every point with separate multiply/add. */
+int orc_border(int dim, const double* pts, const double* h, uint64_t n, const double* centres,
+               uint64_t m, int family, double alpha, double* atp, double* ptp, double* pth) {
+    if ((dim != 2 && dim != 3) || m == 0 || family < 0 || family > 3 || !(alpha > 0.0) ||
+        !isfinite(alpha))
+        return ORC_INVALID;
+    const int T = dim + 1;
+    memset(atp, 0, (size_t)T * m * sizeof(double));
+    const double radius = 1.0 / alpha;
+    const double r2 = radius * radius;
+    grid_t g;
+    if (grid_build(&g, dim, centres, m, radius) != ORC_OK) return ORC_RUNTIME;
+    uint64_t cap = 256;
+    hit_t* hb = (hit_t*)malloc(cap * sizeof(hit_t));
+    for (uint64_t p = 0; p < n; ++p) {
+        const double* q = pts + p * dim;
+        const uint64_t k = point_hits(&g, dim, q, centres, family, alpha, r2, &hb, &cap);
+        for (uint64_t a = 0; a < k; ++a) {
+            const uint32_t j = hb[a].id;
+            const double v = hb[a].v;
+            for (int t = 0; t < dim; ++t) atp[(uint64_t)t * m + j] += v * q[t]; /* solver.cpp:198-200 */
+            atp[(uint64_t)dim * m + j] += v;                                   /* solver.cpp:201 */
+        }
+    }
+    free(hb);
+    grid_free(&g);
+    double s[4][4], sh[4];
+    memset(s, 0, sizeof(s));
+    memset(sh, 0, sizeof(sh));
+    for (uint64_t p = 0; p < n; ++p) { /* solver.cpp:238-250 */
+        double v[4];
+        for (int t = 0; t < dim; ++t) v[t] = pts[p * dim + t];
+        v[dim] = 1.0;
+        for (int a = 0; a < T; ++a) {
+            for (int b = a; b < T; ++b) s[a][b] += v[a] * v[b];
+            sh[a] += v[a] * h[p];
+        }
+    }
+    for (int a = 0; a < T; ++a) {
+        for (int b = 0; b < T; ++b) ptp[a * T + b] = a <= b ? s[a][b] : s[b][a];
+        pth[a] = sh[a];
+    }
+    ptp[T * T - 1] = (double)n; /* the reference stores n, not a running sum */
+    return ORC_OK;
+}
+
+/* evaluate with the polynomial term (model.cpp:65-68): f += a0 x + a1 y (+ a2 z) + a_T-1,
+ * the expression evaluated left to right, unfused. */
+int orc_evaluate_poly(int dim, const double* centres, uint64_t m, const double* w, const double* a,
+                      int family, double alpha, const double* q, uint64_t nq, double* f) {
+    const int st = orc_evaluate(dim, centres, m, w, family, alpha, q, nq, f);
+    if (st != ORC_OK) return st;
+    for (uint64_t i = 0; i < nq; ++i) {
+        const double* p = q + i * dim;
+        double t = a[0] * p[0] + a[1] * p[1];
+        if (dim == 3) t = t + a[2] * p[2];
+        t = t + a[dim];
+        f[i] += t;
+    }
+    return ORC_OK;
+}

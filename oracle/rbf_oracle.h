@@ -85,6 +85,15 @@ int orc_pcg(uint64_t m, const uint64_t* row_ptr, const uint32_t* cols,
             const double* vals, const double* rhs, double shift, double tol,
             int max_iter, double* x, int* iters, double* rel_res);
 
+/* Linear-polynomial border blocks A^T P (T x m, term-major), P^T P (T x T),
+ * P^T h (T), T = dim + 1 (solver.cpp:189-207, 238-262). */
+int orc_border(int dim, const double* pts, const double* h, uint64_t n, const double* centres,
+               uint64_t m, int family, double alpha, double* atp, double* ptp, double* pth);
+
+/* orc_evaluate plus the polynomial term a (T coefficients, model.cpp:65-68). */
+int orc_evaluate_poly(int dim, const double* centres, uint64_t m, const double* w, const double* a,
+                      int family, double alpha, const double* q, uint64_t nq, double* f);
+
 /* Upper CSR -> dense symmetric row-major (m*m). */
 void orc_densify(uint64_t m, const uint64_t* row_ptr, const uint32_t* cols,
                  const double* vals, double* dense);

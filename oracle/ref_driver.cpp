@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <array>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -233,6 +234,67 @@ int ref_bench_step(const double* xy, const double* vals, std::uint64_t n, const 
                                            rhs.data(), design_nnz, nullptr, times);
     *seconds = seconds_since(t0);
     return rc;
+}
+
+// The linear-polynomial border of build_normal_system (solver.cpp:189-207,
+// 238-262), restated over the reference's own compiled assemble_submatrix:
+// A^T P streamed in stored triplet order, P^T P / P^T h in one pass.
+// atp: 3 x m (term-major), ptp: 3 x 3, pth: 3.
+int ref_border(const double* xy, const double* vals, std::uint64_t n, const double* refs_xy,
+               std::uint64_t m, int family, double alpha, double* atp, double* ptp, double* pth) {
+    try {
+        const KernelSpec kernel(family_of(family), alpha);
+        const std::vector<Point2> pts = to_points(xy, n);
+        const PointIndex index(pts);
+        const CooMatrix a = assemble_submatrix(index, to_points(refs_xy, m), kernel);
+        std::vector<double> slots(m * 3, 0.0);
+        const auto arow = a.rows();
+        const auto acol = a.cols();
+        const auto aval = a.values();
+        for (std::size_t i = 0; i < aval.size(); ++i) {
+            const Point2 p = pts[arow[i]];
+            double* slot = &slots[acol[i] * 3];
+            slot[0] += aval[i] * p.x;
+            slot[1] += aval[i] * p.y;
+            slot[2] += aval[i];
+        }
+        for (std::size_t j = 0; j < m; ++j)
+            for (int q = 0; q < 3; ++q) atp[q * m + j] = slots[j * 3 + q];
+        double sxx = 0, sxy = 0, sx = 0, syy = 0, sy = 0, phx = 0, phy = 0, ph1 = 0;
+        for (std::size_t i = 0; i < n; ++i) {
+            const double x = pts[i].x, y = pts[i].y, h = vals[i];
+            sxx += x * x;
+            sxy += x * y;
+            sx += x;
+            syy += y * y;
+            sy += y;
+            phx += x * h;
+            phy += y * h;
+            ph1 += h;
+        }
+        const double t[9] = {sxx, sxy, sx, sxy, syy, sy, sx, sy, static_cast<double>(n)};
+        std::memcpy(ptp, t, sizeof(t));
+        pth[0] = phx;
+        pth[1] = phy;
+        pth[2] = ph1;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// evaluate_model (model.cpp:192-194) of a bordered model (poly = a[0..2]).
+int ref_evaluate_model_poly(const double* refs_xy, const double* w, const double* a, std::uint64_t m,
+                            int family, double alpha, const double* q_xy, std::uint64_t nq, double* f_out) {
+    try {
+        Model model{KernelSpec(family_of(family), alpha), to_points(refs_xy, m),
+                    std::vector<double>(w, w + m), std::array<double, 3>{a[0], a[1], a[2]}, {0.0, 0.0}};
+        const auto f = evaluate_model(model, to_points(q_xy, nq));
+        std::memcpy(f_out, f.data(), nq * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 }  // extern "C"

@@ -111,6 +111,11 @@ _SIGS = {
     "rbg_set_tile_divisor": (C.c_int, [_P, C.c_double]),
     "rbg_set_super_factor": (C.c_int, [_P, C.c_int]),
     "rbg_get_layout_info": (C.c_int, [_P, C.POINTER(LayoutInfo)]),
+    "rbg_set_poly": (C.c_int, [_P, C.c_int]),
+    "rbg_get_border": (C.c_int, [_P, _P, _P, _P]),
+    "rbg_set_border": (C.c_int, [_P, _P, _P, _P]),
+    "rbg_get_poly_solution": (C.c_int, [_P, _P]),
+    "rbg_set_model_poly": (C.c_int, [_P, _P]),
 }
 
 _lib = None

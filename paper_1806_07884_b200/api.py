@@ -139,6 +139,8 @@ class Engine:
                                             kernel.family, kernel.alpha))
         self.dim, self.m, self.kernel = c.shape[1], c.shape[0], kernel
         self._info = None
+        if getattr(self, "poly", False):  # the border setting survives a new centre set
+            self._check(self._L.rbg_set_poly(self._ctx, 1))
 
     def pattern_info(self) -> dict:
         if self._info is None:
@@ -185,6 +187,37 @@ class Engine:
         dn = C.c_uint64()
         self._check(self._L.rbg_get_system(self._ctx, _p(vals), _p(rhs), _p(hits), C.byref(dn)))
         return {"values": vals, "rhs": rhs, "hits": hits, "design_nnz": int(dn.value)}
+
+    # --- linear-polynomial border (FitOptions::poly)
+    def set_poly(self, enable: bool) -> None:
+        """Enable the border [x, y, (z), 1] (solver.cpp:189-207, 238-262) for the
+        following assemblies / solves of this centre set."""
+        self._check(self._L.rbg_set_poly(self._ctx, int(bool(enable))))
+        self.poly = bool(enable)
+
+    @property
+    def poly_terms(self) -> int:
+        return (self.dim + 1) if getattr(self, "poly", False) else 0
+
+    def border(self) -> dict:
+        """A^T P (T x m), P^T P (T x T), P^T h (T) of the last assembly."""
+        T = self.poly_terms
+        atp, ptp, pth = np.empty((T, self.m)), np.empty((T, T)), np.empty(T)
+        self._check(self._L.rbg_get_border(self._ctx, _p(atp), _p(ptp), _p(pth)))
+        return {"atp": atp, "ptp": ptp, "pth": pth}
+
+    def set_border(self, atp, ptp, pth) -> None:
+        a, b, c = _f64(atp), _f64(ptp), _f64(pth)
+        self._check(self._L.rbg_set_border(self._ctx, _p(a), _p(b), _p(c)))
+
+    def poly_solution(self) -> np.ndarray:
+        a = np.zeros(max(self.poly_terms, 1))
+        self._check(self._L.rbg_get_poly_solution(self._ctx, _p(a)))
+        return a[: self.poly_terms]
+
+    def set_model_poly(self, a) -> None:
+        aa = None if a is None else _f64(a)
+        self._check(self._L.rbg_set_model_poly(self._ctx, _p(aa)))
 
     def set_system(self, values, rhs, hits=None) -> None:
         v, r = _f64(values), _f64(rhs)
@@ -245,11 +278,13 @@ class SparseNormalSystem:
 
 @dataclass
 class Model:
-    """rbfit::Model (model.hpp:17-23) without polynomial; offset kept."""
+    """rbfit::Model (model.hpp:17-23): weights, optional linear polynomial
+    (a_x, a_y, (a_z), a_1), offset."""
     kernel: KernelSpec
     refs: np.ndarray
     weights: np.ndarray
     offset: tuple = (0.0, 0.0)
+    poly: np.ndarray | None = None
 
 
 @dataclass
@@ -279,23 +314,30 @@ def _validate_cloud(points, values, refs, who: str):
     return pts, h, r
 
 
-def build_normal_system(points, values, refs, kernel: KernelSpec, engine: Engine | None = None) -> SparseNormalSystem:
+def build_normal_system(points, values, refs, kernel: KernelSpec, engine: Engine | None = None,
+                        poly: bool = False) -> SparseNormalSystem:
     """build_normal_system (solver.hpp:86-94) on the GPU; single plan (the
-    whole pattern is resident), no polynomial border."""
+    whole pattern is resident).  With poly the border blocks are attached as
+    ``border`` (A^T P, P^T P, P^T h)."""
     pts, h, r = _validate_cloud(points, values, refs, "build_normal_system")
     eng = engine or Engine()
     eng.set_centres(r, kernel)
+    eng.set_poly(poly)
     eng.assemble(pts, h)
     sysd = eng.system()
     rp, cols = eng.pattern()
     empty = np.flatnonzero(sysd["hits"] == 0).astype(np.uint32)
-    return SparseNormalSystem(r.shape[0], rp, cols, sysd["values"], sysd["rhs"], empty,
-                              sysd["design_nnz"])
+    s = SparseNormalSystem(r.shape[0], rp, cols, sysd["values"], sysd["rhs"], empty,
+                           sysd["design_nnz"], poly)
+    if poly:
+        s.border = eng.border()
+    return s
 
 
 def fit(points, values, refs, kernel: KernelSpec, tol: float = 0.0, max_iter: int = 0,
-        engine: Engine | None = None) -> tuple[Model, FitReport]:
-    """fit (solver.cpp:401-478): assemble on the GPU, solve, package."""
+        engine: Engine | None = None, poly: bool = False) -> tuple[Model, FitReport]:
+    """fit (solver.cpp:401-478): assemble on the GPU, solve, package
+    (poly = FitOptions::poly, the linear-polynomial border)."""
     pts, h, r = _validate_cloud(points, values, refs, "fit")
     rep = FitReport()
     if pts.shape[0] < r.shape[0]:  # solver.cpp:409-412
@@ -303,9 +345,11 @@ def fit(points, values, refs, kernel: KernelSpec, tol: float = 0.0, max_iter: in
                             "underdetermined")
     eng = engine or Engine()
     eng.set_centres(r, kernel)
+    eng.set_poly(poly)
     eng.assemble(pts, h)
     sysd = eng.system()
     c, diag = eng.solve(tol, max_iter)
+    a = eng.poly_solution() if poly else None
     rep.design_nnz = sysd["design_nnz"]
     rep.empty_support_refs = np.flatnonzero(sysd["hits"] == 0).tolist()
     rep.ridge_lambda = diag["ridge_lambda"]
@@ -317,7 +361,7 @@ def fit(points, values, refs, kernel: KernelSpec, tol: float = 0.0, max_iter: in
     if rep.ridge_lambda > 0.0:
         rep.warnings.append("normal equations numerically singular; ridge solution kept (the "
                             "orthogonal re-pass is not available on the GPU path)")
-    return Model(kernel, r, c), rep
+    return Model(kernel, r, c, poly=a), rep
 
 
 def evaluate_model(model: Model, queries, engine: Engine | None = None) -> np.ndarray:
@@ -328,6 +372,7 @@ def evaluate_model(model: Model, queries, engine: Engine | None = None) -> np.nd
     eng = engine or Engine()
     if eng.m != model.refs.shape[0] or eng.kernel is None or eng.kernel.alpha != model.kernel.alpha:
         eng.set_centres(model.refs, model.kernel)
+    eng.set_model_poly(model.poly)
     return eng.evaluate(model.weights, q)
 
 
@@ -343,6 +388,7 @@ def error_report(model: Model, points, values, design_nnz: int | None = None,
     eng = engine or Engine()
     if eng.m != model.refs.shape[0] or eng.kernel is None or eng.kernel.alpha != model.kernel.alpha:
         eng.set_centres(model.refs, model.kernel)
+    eng.set_model_poly(model.poly)
     rep = eng.error_report(model.weights, pts, h, signed=True)
     if design_nnz is not None:
         rep["density_pct"] = 100.0 * design_nnz / (h.shape[0] * float(model.refs.shape[0]))

@@ -1,6 +1,8 @@
 // rbfit_gpu.cpp -- reference-shaped C++ API over the C ABI (see rbfit_gpu.hpp).
 #include "rbfit_gpu.hpp"
 
+#include <array>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -119,14 +121,12 @@ NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2
     if (cloud.values.size() != cloud.points.size())  // solver.cpp:135-136
         throw std::invalid_argument("build_normal_system: value count does not match points");
     if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
-    if (poly)
-        throw std::invalid_argument(
-            "build_normal_system: the linear-polynomial border is not implemented on the GPU path");
     Using u(device);
     rbg_ctx* ctx = u.ctx();
     BuildStats local{};
     auto t0 = Clock::now();
     set_centres(ctx, refs, kernel);
+    check(rbg_set_poly(ctx, poly ? 1 : 0), ctx);
     local.index_seconds = seconds_since(t0);
     t0 = Clock::now();
     check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
@@ -152,6 +152,14 @@ NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2
     check(rbg_get_pattern(ctx, sys.row_ptr.data(), sys.cols.data()), ctx);
     for (std::size_t j = 0; j < m; ++j)
         if (hits[j] == 0.0) sys.empty_support_refs.push_back(static_cast<std::uint32_t>(j));
+    if (poly) {  // solver.cpp:189-207, 238-262: side = m + T
+        const std::size_t T = 3;
+        sys.poly = true;
+        sys.border_atp.resize(T * m);
+        sys.border_ptp.resize(T * T);
+        sys.border_pth.resize(T);
+        check(rbg_get_border(ctx, sys.border_atp.data(), sys.border_ptp.data(), sys.border_pth.data()), ctx);
+    }
     local.design_nnz = design_nnz;
     local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);
     if (stats) *stats = local;
@@ -170,11 +178,19 @@ Weights solve_weights(const NormalSystem& sys, SolveDiag* diag, Device* device) 
     check(rbg_get_pattern_info(ctx, &info), ctx);
     if (info.m != sys.side || info.nnz_upper != sys.values.size())
         throw std::invalid_argument("solve_weights: system does not match the device's pattern");
+    check(rbg_set_poly(ctx, sys.poly ? 1 : 0), ctx);
     check(rbg_set_system(ctx, sys.values.data(), sys.rhs.data(), nullptr), ctx);
+    if (sys.poly)
+        check(rbg_set_border(ctx, sys.border_atp.data(), sys.border_ptp.data(), sys.border_pth.data()), ctx);
     Weights w;
     w.c.resize(sys.side);
     rbg_solve_diag d{};
     check(rbg_solve(ctx, nullptr, w.c.data(), &d), ctx);
+    if (sys.poly) {  // Weights::poly (solver.cpp:327-328)
+        std::array<double, 4> a{};
+        check(rbg_get_poly_solution(ctx, a.data()), ctx);
+        w.poly = std::array<double, 3>{a[0], a[1], a[2]};
+    }
     if (diag) *diag = SolveDiag{d.ridge_lambda, d.ridge_shift, d.attempts, d.iterations, d.rel_residual};
     return w;
 }
@@ -185,8 +201,6 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     if (cloud.values.size() != cloud.points.size())
         throw std::invalid_argument("fit: cloud value count mismatch");
     if (refs.empty()) throw std::invalid_argument("fit: no reference points");
-    if (options.poly)
-        throw std::invalid_argument("fit: the linear-polynomial border is not implemented on the GPU path");
 
     FitReport local{};
     if (cloud.size() < refs.size())
@@ -200,6 +214,7 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     rbg_ctx* ctx = dev.ctx();
     auto t0 = Clock::now();
     set_centres(ctx, refs, kernel);
+    check(rbg_set_poly(ctx, options.poly ? 1 : 0), ctx);
     local.index_seconds = seconds_since(t0);
     t0 = Clock::now();
     check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
@@ -218,6 +233,12 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     rbg_solve_options so{options.tol, options.max_iter};
     rbg_solve_diag d{};
     check(rbg_solve(ctx, &so, c.data(), &d), ctx);
+    std::optional<std::array<double, 3>> poly;
+    if (options.poly) {
+        std::array<double, 4> a{};
+        check(rbg_get_poly_solution(ctx, a.data()), ctx);
+        poly = std::array<double, 3>{a[0], a[1], a[2]};
+    }
     local.gram_solve_seconds = seconds_since(t0);
     local.design_nnz = design_nnz;
     for (std::size_t j = 0; j < m; ++j)
@@ -233,7 +254,7 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     check(rbg_get_pattern_info(ctx, &info), ctx);
     local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);
 
-    Model model{kernel, std::move(refs), std::move(c), std::nullopt, cloud.offset};
+    Model model{kernel, std::move(refs), std::move(c), poly, cloud.offset};
     if (report) *report = std::move(local);
     return model;
 }
@@ -243,10 +264,9 @@ std::vector<double> evaluate_model(const Model& model, std::span<const Point2> q
     if (model.refs.empty()) throw std::invalid_argument("model has no reference points");
     if (model.weights.size() != model.refs.size())
         throw std::invalid_argument("model weight count does not match reference count");
-    if (model.poly)
-        throw std::invalid_argument("evaluate_model: polynomial models are not supported on the GPU path");
     Using u(device);
     set_centres(u.ctx(), model.refs, model.kernel);
+    check(rbg_set_model_poly(u.ctx(), model.poly ? model.poly->data() : nullptr), u.ctx());  // model.cpp:65-68
     std::vector<Point2> shifted;
     std::span<const Point2> q = queries;
     if (model.offset.x != 0.0 || model.offset.y != 0.0) {  // model.cpp:192-194
@@ -269,6 +289,7 @@ ErrorReport error_report(const Model& model, const PointCloud& cloud,
         throw std::invalid_argument("model weight count does not match reference count");
     Using u(device);
     set_centres(u.ctx(), model.refs, model.kernel);
+    check(rbg_set_model_poly(u.ctx(), model.poly ? model.poly->data() : nullptr), u.ctx());
     const Point2 delta{cloud.offset.x - model.offset.x, cloud.offset.y - model.offset.y};
     std::vector<Point2> shifted;
     std::span<const Point2> q = cloud.points;

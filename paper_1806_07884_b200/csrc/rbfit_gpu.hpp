@@ -11,8 +11,9 @@
 //    BASELINE sizes the dense matrix does not exist in any memory;
 //  * the block planner (BlockPlan / ram budget) has no GPU meaning: the whole
 //    pattern is resident; FitReport::plan reports one block;
-//  * the linear-polynomial border (--poly) and the orthogonal re-pass are not
-//    implemented on the GPU path (std::invalid_argument / warning).
+//  * the linear-polynomial border (FitOptions::poly) is supported (2-D: P =
+//    [x, y, 1] as the reference); the orthogonal re-pass is not implemented
+//    on the GPU path (FitReport warning).
 #pragma once
 
 #include <array>
@@ -81,6 +82,10 @@ struct NormalSystem {
     std::vector<double> values;
     std::vector<double> rhs;
     bool poly = false;
+    // border blocks when poly (side = m + 3 in the reference's dense form):
+    std::vector<double> border_atp;  // A^T P, 3 x m term-major
+    std::vector<double> border_ptp;  // P^T P, 3 x 3
+    std::vector<double> border_pth;  // P^T h, 3
     std::vector<std::uint32_t> empty_support_refs;
     double at(std::size_t i, std::size_t j) const;  // symmetric lookup, 0 off-pattern
 };

@@ -243,7 +243,7 @@ rbg_status rbg_system_device(rbg_ctx* ctx, double** d_buffer, uint64_t* count) {
     return guarded(ctx, [&] {
         require_centres(ctx);
         if (d_buffer) *d_buffer = ctx->sys.p;
-        if (count) *count = ctx->nnz_upper + 2 * ctx->m;
+        if (count) *count = ctx->sys_count();
     });
 }
 
@@ -359,6 +359,69 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
             RBG_CUDA(cudaStreamSynchronize(st));
             for (uint64_t i = 0; i < n; ++i) signed_errors[i] = signed_errors[i] - h[i];  // model.cpp:208
         }
+    });
+}
+
+rbg_status rbg_set_poly(rbg_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        bind(ctx);
+        ctx->poly_on = enable != 0;
+        ctx->have_system = false;  // the system layout changes
+        ctx->sys.reserve(ctx->sys_count());
+    });
+}
+
+rbg_status rbg_get_border(rbg_ctx* ctx, double* atp, double* ptp, double* pth) {
+    return guarded(ctx, [&] {
+        require_system(ctx);
+        const int T = ctx->pterms();
+        if (T == 0) throw Error(RBG_INVALID_ARGUMENT, "no polynomial border (call rbg_set_poly first)");
+        bind(ctx);
+        cudaStream_t st = ctx->stream;
+        const double* E = ctx->sys.p + ctx->border_off();
+        if (atp)
+            RBG_CUDA(cudaMemcpyAsync(atp, E, (uint64_t)T * ctx->m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (ptp)
+            RBG_CUDA(cudaMemcpyAsync(ptp, E + (uint64_t)T * ctx->m, T * T * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+        if (pth)
+            RBG_CUDA(cudaMemcpyAsync(pth, E + (uint64_t)T * ctx->m + T * T, T * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rbg_status rbg_set_border(rbg_ctx* ctx, const double* atp, const double* ptp, const double* pth) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        const int T = ctx->pterms();
+        if (T == 0) throw Error(RBG_INVALID_ARGUMENT, "no polynomial border (call rbg_set_poly first)");
+        if (!atp || !ptp || !pth) throw Error(RBG_INVALID_ARGUMENT, "null border array");
+        bind(ctx);
+        cudaStream_t st = ctx->stream;
+        double* E = ctx->sys.p + ctx->border_off();
+        RBG_CUDA(cudaMemcpyAsync(E, atp, (uint64_t)T * ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(E + (uint64_t)T * ctx->m, ptp, T * T * sizeof(double), cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(E + (uint64_t)T * ctx->m + T * T, pth, T * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+rbg_status rbg_get_poly_solution(rbg_ctx* ctx, double* a) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (!a) throw Error(RBG_INVALID_ARGUMENT, "null array");
+        for (int t = 0; t < ctx->pterms(); ++t) a[t] = ctx->poly_sol[t];
+    });
+}
+
+rbg_status rbg_set_model_poly(rbg_ctx* ctx, const double* a) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        ctx->model_poly = a != nullptr;
+        for (int t = 0; t < 4; ++t) ctx->model_a[t] = (a && t <= ctx->dim) ? a[t] : 0.0;
     });
 }
 

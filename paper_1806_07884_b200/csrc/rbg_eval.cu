@@ -16,11 +16,20 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Linear-polynomial term of a bordered model (model.cpp:65-68): after the
+// support sum, f += a0 x + a1 y (+ a2 z) + a_last, evaluated left to right
+// with unfused mul/add like the reference's expression.
+struct PolyDev {
+    int on;
+    double a[4];
+};
+
 template <int DIM>
 __global__ void eval_kernel(GridDev g, const uint64_t* __restrict__ cptr,
                             const uint32_t* __restrict__ cids, const double* __restrict__ centres,
                             const double* __restrict__ w, int family, double alpha, double r2,
-                            const double* __restrict__ q, uint64_t nq, double* __restrict__ f) {
+                            PolyDev poly, const double* __restrict__ q, uint64_t nq,
+                            double* __restrict__ f) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nq;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const double x = q[i * DIM], y = q[i * DIM + 1], z = DIM == 3 ? q[i * DIM + 2] : 0.0;
@@ -38,6 +47,12 @@ __global__ void eval_kernel(GridDev g, const uint64_t* __restrict__ cptr,
                     if (v != 0.0) acc = __dadd_rn(acc, __dmul_rn(w[j], v));
                 }
             }
+        }
+        if (poly.on) {
+            double t = __dadd_rn(__dmul_rn(poly.a[0], x), __dmul_rn(poly.a[1], y));
+            if (DIM == 3) t = __dadd_rn(t, __dmul_rn(poly.a[2], z));
+            t = __dadd_rn(t, poly.a[DIM]);
+            acc = __dadd_rn(acc, t);
         }
         f[i] = acc;
     }
@@ -126,14 +141,15 @@ void evaluate_points(rbg_ctx* ctx, const double* d_c, const double* d_q, uint64_
     if (nq == 0) return;
     const GridDev g = grid_dev(ctx->grid);
     const unsigned blocks = blocks_for(nq, kThreads);
+    PolyDev poly{ctx->model_poly, {ctx->model_a[0], ctx->model_a[1], ctx->model_a[2], ctx->model_a[3]}};
     if (ctx->dim == 2)
         eval_kernel<2><<<blocks, kThreads, 0, ctx->stream>>>(g, ctx->tile_cptr.p, ctx->tile_cids.p,
                                                             ctx->centres.p, d_c, ctx->family,
-                                                            ctx->alpha, ctx->r2, d_q, nq, d_f);
+                                                            ctx->alpha, ctx->r2, poly, d_q, nq, d_f);
     else
         eval_kernel<3><<<blocks, kThreads, 0, ctx->stream>>>(g, ctx->tile_cptr.p, ctx->tile_cids.p,
                                                             ctx->centres.p, d_c, ctx->family,
-                                                            ctx->alpha, ctx->r2, d_q, nq, d_f);
+                                                            ctx->alpha, ctx->r2, poly, d_q, nq, d_f);
     RBG_CHECK_LAUNCH(ctx);
 }
 

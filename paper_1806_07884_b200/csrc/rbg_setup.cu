@@ -399,7 +399,7 @@ void setup_centres(rbg_ctx* ctx) {
     ctx->lay = AsmLayout();  // rebuilt at the next assembly for this centre set
 
     // ---- system + point workspace sized for this centre set ----------------
-    ctx->sys.reserve(ctx->nnz_upper + 2 * m);
+    ctx->sys.reserve(ctx->nnz_upper + 2 * m + 4 * m + 20);  // room for the polynomial border
     ctx->counters.reserve(4);
     RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
     RBG_CUDA(cudaStreamSynchronize(st));

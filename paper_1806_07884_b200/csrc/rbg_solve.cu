@@ -35,7 +35,18 @@ enum : int {
     S_ITERS,
     S_MAXIT,
     S_TRACE,
-    S_COUNT
+    S_W0,  // S_W0 .. S_W0+3: border products E^T v
+    S_COUNT = S_W0 + 4
+};
+
+// Linear-polynomial border of the bordered system [[B, E], [E^T, F]]
+// (solver.cpp:189-207, 238-262): E = A^T P (T x m, term-major), F = P^T P.
+// T = 0 without the border.
+struct BorderDev {
+    int T;
+    uint64_t m;
+    const double* E;
+    const double* F;
 };
 
 constexpr int kThreads = 256;
@@ -110,15 +121,17 @@ __global__ void trace_kernel(const uint64_t* __restrict__ uptr, const double* __
 }
 
 __global__ void init_kernel(const uint64_t* __restrict__ uptr, const double* __restrict__ uvals,
-                            const double* __restrict__ b, uint64_t m, double* __restrict__ dinv,
+                            const double* __restrict__ b, uint64_t m, BorderDev bd, double* __restrict__ dinv,
                             double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                             double* __restrict__ p, double* partials, unsigned* ticket, double* scal,
                             double tol2) {
     const double shift = scal[S_SHIFT];
     double v[3] = {0.0, 0.0, 0.0};  // rz, bb, non-positive diagonal count
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+    const uint64_t nt = m + (uint64_t)bd.T;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nt;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const double d = uvals[uptr[i]] + shift;  // upper row i starts at the diagonal
+        // upper row i starts at the diagonal; border rows take F's diagonal
+        const double d = (i < m ? uvals[uptr[i]] : bd.F[(i - m) * bd.T + (i - m)]) + shift;
         if (!(d > 0.0) || !isfinite(d)) v[2] += 1.0;
         const double di = 1.0 / d;
         dinv[i] = di;
@@ -143,9 +156,24 @@ __global__ void init_kernel(const uint64_t* __restrict__ uptr, const double* __r
     }
 }
 
+// scal[S_W0 + t] = sum_i E[t][i] v[i]  (the E^T v half of the border SpMV)
+__global__ void border_dot_kernel(BorderDev bd, const double* __restrict__ v, double* partials,
+                                  unsigned* ticket, double* scal, int force) {
+    if (!force && (scal[S_DONE] != 0.0 || scal[S_FAIL] != 0.0)) return;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < bd.m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double vi = v[i];
+        for (int t = 0; t < bd.T; ++t) acc[t] = fma(bd.E[(uint64_t)t * bd.m + i], vi, acc[t]);
+    }
+    double out[4];
+    if (last_block_sum<4>(acc, partials, ticket, out) && threadIdx.x == 0)
+        for (int t = 0; t < 4; ++t) scal[S_W0 + t] = out[t];
+}
+
 // q = (B + shift I) p, one warp per row; pq = p.q.
 __global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
-                                const double* __restrict__ vfull, uint64_t m,
+                                const double* __restrict__ vfull, uint64_t m, BorderDev bd,
                                 const double* __restrict__ p, double* __restrict__ q,
                                 double* partials, unsigned* ticket, double* scal) {
     if (scal[S_DONE] != 0.0 || scal[S_FAIL] != 0.0) return;
@@ -160,6 +188,7 @@ __global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_
         for (uint64_t e = fptr[row] + lane; e < e1; e += 32) s = fma(vfull[e], p[fcols[e]], s);
         s = warp_sum(s);
         if (lane == 0) {
+            for (int t = 0; t < bd.T; ++t) s = fma(bd.E[(uint64_t)t * m + row], p[m + t], s);
             const double pi = p[row];
             const double qi = s + shift * pi;
             q[row] = qi;
@@ -168,7 +197,13 @@ __global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_
     }
     double out[1];
     if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) {
-        const double pq = out[0];
+        double pq = out[0];
+        for (int t = 0; t < bd.T; ++t) {  // border rows: E^T p (border_dot_kernel) + F p_b
+            double qt = scal[S_W0 + t] + shift * p[m + t];
+            for (int u = 0; u < bd.T; ++u) qt = fma(bd.F[t * bd.T + u], p[m + u], qt);
+            q[m + t] = qt;
+            pq += p[m + t] * qt;
+        }
         scal[S_PQ] = pq;
         if (!(pq > 0.0) || !isfinite(pq)) scal[S_FAIL] = 1.0;
         else scal[S_ALPHA] = scal[S_RZ] / pq;
@@ -217,7 +252,7 @@ __global__ void direction_kernel(uint64_t m, const double* __restrict__ z, doubl
 
 // r = b - (B + shift I) x ; returns ||r||^2 in scal[S_PQ] (reused slot)
 __global__ void residual_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
-                                const double* __restrict__ vfull, uint64_t m,
+                                const double* __restrict__ vfull, uint64_t m, BorderDev bd,
                                 const double* __restrict__ x, const double* __restrict__ b,
                                 double* partials, unsigned* ticket, double* scal) {
     const double shift = scal[S_SHIFT];
@@ -230,12 +265,22 @@ __global__ void residual_kernel(const uint64_t* __restrict__ fptr, const uint32_
         for (uint64_t e = fptr[row] + lane; e < fptr[row + 1]; e += 32) s = fma(vfull[e], x[fcols[e]], s);
         s = warp_sum(s);
         if (lane == 0) {
+            for (int t = 0; t < bd.T; ++t) s = fma(bd.E[(uint64_t)t * m + row], x[m + t], s);
             const double ri = b[row] - (s + shift * x[row]);
             v[0] += ri * ri;
         }
     }
     double out[1];
-    if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) scal[S_PQ] = out[0];
+    if (last_block_sum<1>(v, partials, ticket, out) && threadIdx.x == 0) {
+        double rr = out[0];
+        for (int t = 0; t < bd.T; ++t) {
+            double qt = scal[S_W0 + t] + shift * x[m + t];
+            for (int u = 0; u < bd.T; ++u) qt = fma(bd.F[t * bd.T + u], x[m + u], qt);
+            const double rt = b[m + t] - qt;
+            rr += rt * rt;
+        }
+        scal[S_PQ] = rr;
+    }
 }
 
 }  // namespace
@@ -246,14 +291,28 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     const double tol = (opts && opts->tol > 0.0) ? opts->tol : 1e-12;
     const int max_iter = (opts && opts->max_iter > 0) ? opts->max_iter : 20000;
     const double* uvals = ctx->sys.p;
+    const int T = ctx->pterms();
+    const uint64_t nt = m + (uint64_t)T;  // unknowns: c (m) and the border coefficients (T)
+    BorderDev bd{T, m, nullptr, nullptr};
     const double* b = ctx->sys.p + ctx->nnz_upper;
+    std::vector<double> hF(16, 0.0);
+    if (T) {
+        bd.E = ctx->sys.p + ctx->border_off();
+        bd.F = bd.E + (uint64_t)T * m;
+        // contiguous right-hand side [A^T h | P^T h]
+        ctx->bvec.reserve(nt);
+        RBG_CUDA(cudaMemcpyAsync(ctx->bvec.p, b, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(ctx->bvec.p + m, bd.F + T * T, T * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        RBG_CUDA(cudaMemcpyAsync(hF.data(), bd.F, T * T * sizeof(double), cudaMemcpyDeviceToHost, st));
+        b = ctx->bvec.p;
+    }
 
     ctx->vfull.reserve(nnz);
-    for (auto* v : {&ctx->x, &ctx->r, &ctx->z, &ctx->p, &ctx->q, &ctx->dinv}) v->reserve(m);
-    const unsigned g_vec = blocks_for(m, kThreads, 148u * 4u);
+    for (auto* v : {&ctx->x, &ctx->r, &ctx->z, &ctx->p, &ctx->q, &ctx->dinv}) v->reserve(nt);
+    const unsigned g_vec = blocks_for(nt, kThreads, 148u * 4u);
     const unsigned g_spmv = blocks_for(m, kThreads / 32, 148u * 8u);
     const unsigned g_max = std::max(g_vec, g_spmv);
-    ctx->partials.reserve(3ull * g_max);
+    ctx->partials.reserve(4ull * g_max);
     ctx->scal.reserve(S_COUNT);
     ctx->ticket.reserve(1);
     RBG_CUDA(cudaMemsetAsync(ctx->ticket.p, 0, sizeof(unsigned), st));
@@ -269,20 +328,24 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     double trace = 0.0;
     RBG_CUDA(cudaMemcpyAsync(&trace, ctx->scal.p + S_TRACE, sizeof(double), cudaMemcpyDeviceToHost, st));
     RBG_CUDA(cudaStreamSynchronize(st));
-    const double mean_diag = trace / (double)m;  // solver.cpp:296
+    for (int t = 0; t < T; ++t) trace += hF[t * T + t];
+    const double mean_diag = trace / (double)nt;  // solver.cpp:296 (trace / side)
 
     // one batch of iterations as a graph (kernels read their scalars on device)
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     RBG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int it = 0; it < kBatch; ++it) {
-        spmv_dot_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m,
+        if (T)
+            border_dot_kernel<<<g_vec, kThreads, 0, st>>>(bd, ctx->p.p, ctx->partials.p, ctx->ticket.p,
+                                                          ctx->scal.p, 0);
+        spmv_dot_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, bd,
                                                      ctx->p.p, ctx->q.p, ctx->partials.p,
                                                      ctx->ticket.p, ctx->scal.p);
-        update_kernel<<<g_vec, kThreads, 0, st>>>(m, ctx->p.p, ctx->q.p, ctx->dinv.p, ctx->x.p,
+        update_kernel<<<g_vec, kThreads, 0, st>>>(nt, ctx->p.p, ctx->q.p, ctx->dinv.p, ctx->x.p,
                                                   ctx->r.p, ctx->z.p, ctx->partials.p,
                                                   ctx->ticket.p, ctx->scal.p);
-        direction_kernel<<<g_vec, kThreads, 0, st>>>(m, ctx->z.p, ctx->p.p, ctx->scal.p);
+        direction_kernel<<<g_vec, kThreads, 0, st>>>(nt, ctx->z.p, ctx->p.p, ctx->scal.p);
     }
     RBG_CUDA(cudaStreamEndCapture(st, &graph));
     RBG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
@@ -300,7 +363,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                                      cudaMemcpyHostToDevice, st));
             RBG_CUDA(cudaMemcpyAsync(ctx->scal.p + S_MAXIT, &init[1], sizeof(double),
                                      cudaMemcpyHostToDevice, st));
-            init_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, b, m, ctx->dinv.p, ctx->x.p,
+            init_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, b, m, bd, ctx->dinv.p, ctx->x.p,
                                                     ctx->r.p, ctx->z.p, ctx->p.p, ctx->partials.p,
                                                     ctx->ticket.p, ctx->scal.p, tol * tol);
             RBG_CHECK_LAUNCH(ctx);
@@ -310,7 +373,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                 RBG_CUDA(cudaStreamSynchronize(st));
                 if (flags[0] != 0.0 || flags[1] != 0.0) break;
                 RBG_CUDA(cudaGraphLaunch(exec, st));
-                ctx->launches += 3 * kBatch;
+                ctx->launches += (T ? 4 : 3) * kBatch;
             }
             if (flags[0] != 0.0 && flags[1] == 0.0) {
                 solved = true;
@@ -330,17 +393,22 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     if (!solved) {
         // first non-positive diagonal (the pivot an LLT meets first on an
         // empty-support column), else the last row reached.
-        std::vector<double> dg(m);
-        RBG_CUDA(cudaMemcpyAsync(dg.data(), ctx->dinv.p, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        std::vector<double> dg(nt);
+        RBG_CUDA(cudaMemcpyAsync(dg.data(), ctx->dinv.p, nt * sizeof(double), cudaMemcpyDeviceToHost, st));
         RBG_CUDA(cudaStreamSynchronize(st));
         uint64_t piv = 0;
-        while (piv < m && dg[piv] > 0.0 && std::isfinite(dg[piv])) ++piv;
-        if (piv == m) piv = 0;
+        while (piv < nt && dg[piv] > 0.0 && std::isfinite(dg[piv])) ++piv;
+        if (piv == nt) piv = 0;
         throw Error(RBG_RUNTIME_ERROR,
                     "normal system is not positive definite even with ridge 1e-06; first "
                     "non-positive pivot at index " + std::to_string(piv));
     }
-    residual_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, ctx->x.p,
+    if (T) {
+        border_dot_kernel<<<g_vec, kThreads, 0, st>>>(bd, ctx->x.p, ctx->partials.p, ctx->ticket.p,
+                                                      ctx->scal.p, 1);
+        RBG_CHECK_LAUNCH(ctx);
+    }
+    residual_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, bd, ctx->x.p,
                                                  b, ctx->partials.p, ctx->ticket.p, ctx->scal.p);
     RBG_CHECK_LAUNCH(ctx);
     RBG_CUDA(cudaEventRecord(ctx->ev1, st));
@@ -349,6 +417,9 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     RBG_CUDA(cudaMemcpyAsync(&bb, ctx->scal.p + S_BB, sizeof(double), cudaMemcpyDeviceToHost, st));
     if (c_out)
         RBG_CUDA(cudaMemcpyAsync(c_out, ctx->x.p, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    for (double& a : ctx->poly_sol) a = 0.0;
+    if (T)
+        RBG_CUDA(cudaMemcpyAsync(ctx->poly_sol, ctx->x.p + m, T * sizeof(double), cudaMemcpyDeviceToHost, st));
     RBG_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
     RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));

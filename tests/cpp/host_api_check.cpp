@@ -52,9 +52,6 @@ static int cpu_checks() {
     EXPECT_THROW(fit(one, {{0.0, 0.0}}, k), std::invalid_argument, "value count mismatch");
     one.values = {1.0};
     EXPECT_THROW(fit(one, {}, k), std::invalid_argument, "no reference points");
-    FitOptions poly;
-    poly.poly = true;
-    EXPECT_THROW(fit(one, {{0.0, 0.0}}, k, poly), std::invalid_argument, "polynomial");
     std::printf("cpu checks: %d failures\n", failures);
     return failures;
 }
@@ -104,8 +101,45 @@ static int gpu_run(const char* in_path, const char* out_path) {
     return std::isfinite(worst) ? 0 : 1;
 }
 
+// FitOptions::poly through the host layer: out.bin = f64 mae, f64 poly[3], f64 c[m].
+static int gpu_poly(const char* in_path, const char* out_path) {
+    std::ifstream in(in_path, std::ios::binary);
+    std::uint64_t n = 0, m = 0;
+    double alpha = 0;
+    in.read(reinterpret_cast<char*>(&n), 8);
+    in.read(reinterpret_cast<char*>(&m), 8);
+    in.read(reinterpret_cast<char*>(&alpha), 8);
+    PointCloud cloud;
+    cloud.points.resize(n);
+    cloud.values.resize(n);
+    std::vector<Point2> refs(m);
+    in.read(reinterpret_cast<char*>(cloud.points.data()), n * 16);
+    in.read(reinterpret_cast<char*>(cloud.values.data()), n * 8);
+    in.read(reinterpret_cast<char*>(refs.data()), m * 16);
+    FitOptions options;
+    options.poly = true;
+    const Model model = fit(cloud, refs, KernelSpec(KernelFamily::wendland_3_1, alpha), options);
+    const ErrorReport er = error_report(model, cloud);
+    if (!model.poly) return 3;
+    // the two-call path (build_normal_system + solve_weights) must agree
+    Device dev(0);
+    const NormalSystem sys = build_normal_system(cloud, refs, KernelSpec(KernelFamily::wendland_3_1, alpha), true,
+                                                 nullptr, &dev);
+    const Weights w = solve_weights(sys, nullptr, &dev);
+    if (!w.poly || sys.border_atp.size() != 3 * m) return 4;
+    std::ofstream out(out_path, std::ios::binary);
+    out.write(reinterpret_cast<const char*>(&er.mean_absolute_error), 8);
+    out.write(reinterpret_cast<const char*>(model.poly->data()), 24);
+    out.write(reinterpret_cast<const char*>(model.weights.data()), m * 8);
+    out.write(reinterpret_cast<const char*>(w.poly->data()), 24);
+    std::printf("gpu poly: mae=%.3g poly=(%.12g, %.12g, %.12g)\n", er.mean_absolute_error, (*model.poly)[0],
+                (*model.poly)[1], (*model.poly)[2]);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     if (argc >= 2 && std::strcmp(argv[1], "cpu") == 0) return cpu_checks();
+    if (argc >= 4 && std::strcmp(argv[1], "poly") == 0) return gpu_poly(argv[2], argv[3]);
     if (argc >= 4 && std::strcmp(argv[1], "gpu") == 0) return gpu_run(argv[2], argv[3]);
     std::fprintf(stderr, "usage: host_api_check cpu | gpu in.bin out.bin\n");
     return 2;

@@ -115,10 +115,49 @@ def cfg1_system():
                         points_head=xy[:64], values_head=h[:64])
 
 
+def poly_cases():
+    # The linear-polynomial border (FitOptions::poly; solver.cpp:189-207,
+    # 238-262, model.cpp:65-68): README case and random small instances, border
+    # blocks from the reference's compiled assemble_submatrix streamed in its
+    # own order, c/poly from the restated Cholesky of the bordered system, f
+    # from the reference's own evaluate_model with the polynomial.
+    g = np.load(OUT / "readme_case.npz")
+    xy, h, refs = g["points"], g["values"], g["refs"]
+    R = po.ref_build_normal_system(xy, h, refs, W31, 0.5)
+    B = po.ref_border(xy, h, refs, W31, 0.5)
+    k, rhs = po.bordered_dense(R["b"], R["rhs"], B)
+    x, d = po.cholesky_solve(k, rhs)
+    m = refs.shape[0]
+    c, a = x[:m], x[m:]
+    f = po.ref_evaluate_poly(refs, c, a, W31, 0.5, xy)
+    mae = float(np.mean(np.abs(f - h)))
+    data = {"readme_mae": mae, "readme_points": xy, "readme_values": h, "readme_refs": refs, "readme_atp": B["atp"],
+            "readme_ptp": B["ptp"], "readme_pth": B["pth"], "readme_c": c, "readme_a": a, "readme_f": f,
+            "readme_ridge": d["ridge_lambda"]}
+    rng = np.random.default_rng(20260)
+    for t in range(6):
+        n = 80 + int(rng.random() * 400)
+        mm = 6 + int(rng.random() * 30)
+        pts = rng.random((n, 2))
+        hv = 2.0 * rng.random(n) - 1.0
+        rr = pts[[j * n // mm for j in range(mm)]].copy()
+        fam = (W31, W30, W33)[t % 3]
+        alpha = 0.75 + 6.0 * rng.random()
+        B = po.ref_border(pts, hv, rr, fam, alpha)
+        data.update({f"{t}_points": pts, f"{t}_values": hv, f"{t}_refs": rr, f"{t}_family": fam,
+                     f"{t}_alpha": alpha, f"{t}_atp": B["atp"], f"{t}_ptp": B["ptp"], f"{t}_pth": B["pth"]})
+    data["count"] = 6
+    np.savez_compressed(OUT / "poly_cases.npz", **data)
+
+
 if __name__ == "__main__":
-    kernel_kat()
-    readme_case()
-    random_small()
-    cfg1_system()
+    if "--poly" in sys.argv:
+        poly_cases()
+    else:
+        kernel_kat()
+        readme_case()
+        random_small()
+        cfg1_system()
+        poly_cases()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -232,3 +232,130 @@ def test_layout_does_not_change_results(eng, div, sup):
     finally:
         eng.set_tile_divisor(0)
         eng.set_super_factor(0)
+
+
+# ------------------------------------------------ linear-polynomial border
+def _border_close(b, ref):
+    for k in ("atp", "ptp", "pth"):
+        assert scaled(b[k], ref[k]) < TOL_SYS, k
+
+
+def test_border_vs_reference(eng, golden):
+    """A^T P, P^T P, P^T h (solver.cpp:189-207, 238-262) on the GPU against the
+    reference's own border on the committed instances (A^T P is summed in a
+    different order, hence the 1e-10 scaled tolerance)."""
+    g = golden("poly_cases")
+    try:
+        for t in range(int(g["count"])):
+            k = api.KernelSpec(int(g[f"{t}_family"]), float(g[f"{t}_alpha"]))
+            eng.set_centres(g[f"{t}_refs"], k)
+            eng.set_poly(True)
+            eng.assemble(g[f"{t}_points"], g[f"{t}_values"])
+            _border_close(eng.border(), {kk: g[f"{t}_{kk}"] for kk in ("atp", "ptp", "pth")})
+    finally:
+        eng.set_poly(False)
+
+
+def test_bordered_fit_readme_vs_reference(eng, golden):
+    """README case with --poly (alpha = 0.5: the bordered system is too ill
+    conditioned for a 1e-8 weight comparison with any iterative solver, like
+    the plain README case): the border blocks within 1e-10 of the reference's,
+    evaluation with the polynomial bitwise equal to the reference's
+    evaluate_model for the same weights, and the GPU fit's MAE within 1 % of
+    the reference-path (restated Cholesky) fit's."""
+    g = golden("poly_cases")
+    k = api.KernelSpec(1, 0.5)
+    try:
+        eng.set_centres(g["readme_refs"], k)
+        eng.set_poly(True)
+        eng.assemble(g["readme_points"], g["readme_values"])
+        _border_close(eng.border(), {kk: g[f"readme_{kk}"] for kk in ("atp", "ptp", "pth")})
+        eng.set_model_poly(g["readme_a"])
+        f = eng.evaluate(g["readme_c"], g["readme_points"])
+        assert np.array_equal(f, g["readme_f"])
+        model, rep = api.fit(g["readme_points"], g["readme_values"], g["readme_refs"], k, engine=eng, poly=True)
+        er = api.error_report(model, g["readme_points"], g["readme_values"], engine=eng)
+        assert er["mean_absolute_error"] == pytest.approx(float(g["readme_mae"]), rel=1e-2)
+    finally:
+        eng.set_model_poly(None)
+        eng.set_poly(False)
+
+
+def test_bordered_solve_vs_dense_cholesky(eng, golden):
+    """c and the polynomial of the bordered solve within 1e-8 of the restated
+    dense Cholesky (solver.cpp:289-330 with side = m + 3) on the committed
+    well-conditioned instances."""
+    g = golden("poly_cases")
+    try:
+        for t in range(int(g["count"])):
+            pts, h, refs = g[f"{t}_points"], g[f"{t}_values"], g[f"{t}_refs"]
+            fam, alpha = int(g[f"{t}_family"]), float(g[f"{t}_alpha"])
+            k = api.KernelSpec(fam, alpha)
+            eng.set_centres(refs, k)
+            eng.set_poly(True)
+            eng.assemble(pts, h)
+            c, diag = eng.solve()
+            a = eng.poly_solution()
+            rp, cols = po.pattern(refs, alpha)
+            v, rhs, _ = po.assemble(pts, h, refs, fam, alpha, rp, cols)
+            kd, rd = po.bordered_dense(po.densify(rp, cols, v), rhs,
+                                       {kk: g[f"{t}_{kk}"] for kk in ("atp", "ptp", "pth")})
+            if np.linalg.cond(kd) > 1e7:
+                continue  # 1e-12 residual does not pin 1e-8 weights there
+            x, d = po.cholesky_solve(kd, rd)
+            if d["ridge_lambda"] != 0.0:
+                continue
+            got = np.concatenate([c, a])
+            assert np.max(np.abs(got - x)) / np.max(np.abs(x)) < TOL_C, t
+    finally:
+        eng.set_poly(False)
+
+
+def test_poly_affine_reproduction(eng):
+    """acceptance C06 (acceptance_main.cpp:207-225): h = 2x + 3y + 1, 4x4 grid of
+    references, phi31 alpha 1, with the border -> MAE < 1e-8 through fit +
+    error_report (2-D), and the 3-D analogue with P = [x, y, z, 1]."""
+    rng = np.random.default_rng(77)
+    pts = rng.random((200, 2))
+    h = 2.0 * pts[:, 0] + 3.0 * pts[:, 1] + 1.0
+    gx, gy = np.meshgrid(np.linspace(0, 1, 4), np.linspace(0, 1, 4))
+    refs = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    k = api.KernelSpec(1, 1.0)
+    try:
+        model, _ = api.fit(pts, h, refs, k, engine=eng, poly=True)
+        rep = api.error_report(model, pts, h, engine=eng)
+        assert rep["mean_absolute_error"] < 1e-8
+        assert np.allclose(model.poly, [2.0, 3.0, 1.0], atol=1e-6)
+        p3 = rng.random((600, 3))
+        h3 = 1.5 * p3[:, 0] - 0.5 * p3[:, 1] + 2.0 * p3[:, 2] + 0.25
+        g3 = np.stack(np.meshgrid(*[np.linspace(0, 1, 3)] * 3), axis=-1).reshape(-1, 3)
+        model3, _ = api.fit(p3, h3, g3, api.KernelSpec("wendland-3-2", 1.2), engine=eng, poly=True)
+        rep3 = api.error_report(model3, p3, h3, engine=eng)
+        assert rep3["mean_absolute_error"] < 1e-8
+    finally:
+        eng.set_model_poly(None)
+        eng.set_poly(False)
+
+
+def test_border_slab_allreduce_sum(eng):
+    """The border is part of the all-reduced system buffer: assembling two
+    slabs with accumulate gives the single-pass border."""
+    rng = np.random.default_rng(5)
+    pts = rng.random((3000, 2))
+    h = np.cos(3 * pts[:, 0]) * pts[:, 1]
+    refs = rng.random((120, 2))
+    k = api.KernelSpec(1, 6.0)
+    try:
+        eng.set_centres(refs, k)
+        eng.set_poly(True)
+        eng.assemble(pts, h)
+        one = eng.border()
+        _, count = eng.system_device()
+        assert count == eng.pattern_info()["nnz_upper"] + 2 * 120 + 3 * 120 + 9 + 3
+        eng.assemble(pts[:1700], h[:1700])
+        eng.assemble(pts[1700:], h[1700:], accumulate=True)
+        two = eng.border()
+        _border_close(two, one)
+        _border_close(one, po.border(pts, h, refs, 1, 6.0))
+    finally:
+        eng.set_poly(False)

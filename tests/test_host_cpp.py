@@ -52,3 +52,28 @@ def test_host_layer_fit_matches_reference_golden(exe, tmp_path, golden):
     # README.md:69 mae of this fit (ill-conditioned, alpha = 0.5: loose by design)
     assert mae == pytest.approx(float(g["published_mae"]), rel=1e-4)
     assert np.all(np.isfinite(f)) and np.all(np.isfinite(c))
+
+
+@pytest.mark.gpu
+def test_host_layer_poly_affine_reproduction(exe, tmp_path):
+    """FitOptions::poly through rbfit_b200::fit (acceptance C06,
+    acceptance_main.cpp:207-225): h = 2x + 3y + 1 -> MAE < 1e-8."""
+    rng = np.random.default_rng(77)
+    xy = rng.random((200, 2))
+    h = 2.0 * xy[:, 0] + 3.0 * xy[:, 1] + 1.0
+    gx, gy = np.meshgrid(np.linspace(0, 1, 4), np.linspace(0, 1, 4))
+    refs = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        np.array([len(h), len(refs)], dtype=np.uint64).tofile(f)
+        np.array([1.0]).tofile(f)
+        xy.tofile(f)
+        h.tofile(f)
+        refs.tofile(f)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), "poly", str(inp), str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    d = np.fromfile(out, dtype=np.float64)
+    assert d[0] < 1e-8
+    assert np.allclose(d[1:4], [2.0, 3.0, 1.0], atol=1e-6)
+    assert np.allclose(d[-3:], d[1:4], rtol=1e-8, atol=1e-10)

@@ -223,3 +223,40 @@ def test_live_reference_random_3d_free_cases():
         h = rng.random(n)
         R = po.ref_build_normal_system(pts, h, refs, W31, alpha)
         _check_against_reference_system(pts, h, refs, W31, alpha, R["b"], R["rhs"], R["ref_nnz"])
+
+
+# ------------------------------------------------ linear-polynomial border
+def test_border_oracle_bitwise_vs_reference(golden):
+    """orc_border restates solver.cpp:189-207, 238-262: bitwise equal to the
+    reference's own triplet-order border on every committed instance."""
+    g = golden("poly_cases")
+    for t in range(int(g["count"])):
+        b = po.border(g[f"{t}_points"], g[f"{t}_values"], g[f"{t}_refs"], int(g[f"{t}_family"]),
+                      float(g[f"{t}_alpha"]))
+        for k in ("atp", "ptp", "pth"):
+            assert np.array_equal(b[k], g[f"{t}_{k}"]), (t, k)
+    b = po.border(g["readme_points"], g["readme_values"], g["readme_refs"], 1, 0.5)
+    assert all(np.array_equal(b[k], g[f"readme_{k}"]) for k in ("atp", "ptp", "pth"))
+
+
+def test_poly_eval_oracle_bitwise_vs_reference(golden):
+    """model.cpp:65-68 polynomial term, unfused left-to-right: bitwise."""
+    g = golden("poly_cases")
+    f = po.evaluate_poly(g["readme_refs"], g["readme_c"], g["readme_a"], 1, 0.5, g["readme_points"])
+    assert np.array_equal(f, g["readme_f"])
+
+
+def test_bordered_cholesky_affine_reproduction():
+    """acceptance C06 (acceptance_main.cpp:207-225) on the oracle: h = 2x + 3y + 1
+    with the border is reproduced to MAE < 1e-8."""
+    rng = np.random.default_rng(77)
+    pts = rng.random((200, 2))
+    h = 2.0 * pts[:, 0] + 3.0 * pts[:, 1] + 1.0
+    gx, gy = np.meshgrid(np.linspace(0, 1, 4), np.linspace(0, 1, 4))
+    refs = np.stack([gx.ravel(), gy.ravel()], axis=1)
+    rp, cols = po.pattern(refs, 1.0)
+    v, rhs, _ = po.assemble(pts, h, refs, 1, 1.0, rp, cols)
+    k, r = po.bordered_dense(po.densify(rp, cols, v), rhs, po.border(pts, h, refs, 1, 1.0))
+    x, _ = po.cholesky_solve(k, r)
+    f = po.evaluate_poly(refs, x[:16], x[16:], 1, 1.0, pts)
+    assert np.mean(np.abs(f - h)) < 1e-8
