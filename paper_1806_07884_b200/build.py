@@ -27,8 +27,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
                      f"-I{ROOT / 'include'}"]
-CU_SOURCES = ["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu", "rbg_solve.cu",
-              "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu"]
+# the assembly kernels are split one translation unit per (dimension, family) so they compile in parallel
+CU_SOURCES = (["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu", "rbg_solve.cu",
+               "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu"]
+              + [f"rbg_asm_part_{d}_{f}.cu" for d in (2, 3) for f in range(4)])
 
 LIB_RBG = PKG / "librbg.so"
 LIB_HOST = PKG / "librbfit_b200.so"
@@ -60,7 +62,7 @@ def build_rbg(force: bool = False, ptxas_verbose: bool = False) -> Path:
         if force or _stale(o, [s] + headers):
             extra = ["-Xptxas", "-v"] if ptxas_verbose else []
             jobs.append([NVCC, *NVCC_FLAGS, *extra, "-c", str(s), "-o", str(o)])
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=max(4, os.cpu_count() or 4)) as ex:
         list(ex.map(_run, jobs))
     objs = [OBJ / (Path(s).stem + ".o") for s in CU_SOURCES]
     if force or jobs or _stale(LIB_RBG, objs):

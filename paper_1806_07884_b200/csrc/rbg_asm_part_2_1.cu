@@ -1,0 +1,6 @@
+// Assembly kernels for dimension 2, kernel family 1 (rbg_kernel_family, include/rbg.h).
+#include "rbg_asm.cuh"
+
+namespace rbg {
+RBG_ASM_DEFINE(2, 1)
+}  // namespace rbg

@@ -1,0 +1,6 @@
+// Assembly kernels for dimension 3, kernel family 0 (rbg_kernel_family, include/rbg.h).
+#include "rbg_asm.cuh"
+
+namespace rbg {
+RBG_ASM_DEFINE(3, 0)
+}  // namespace rbg
