@@ -26,7 +26,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
-                     f"-I{ROOT / 'include'}"]
+                     f"-I{ROOT / 'include'}"] + os.environ.get("RBG_NVCC_EXTRA", "").split()
 # the assembly kernels are split one translation unit per (dimension, family) so they compile in parallel
 CU_SOURCES = (["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu", "rbg_solve.cu",
                "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu"]

@@ -278,6 +278,10 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     constexpr int nsc = (int)std::size(kSubCaps), nlc = (int)std::size(kSuperCaps);
     std::vector<std::vector<uint32_t>> lists(nsc * nlc);
     std::vector<uint32_t> fb;
+    // work estimate per super-tile (register SYRK blocks summed over its
+    // sub-tiles): the work counter hands out the heaviest super-tiles first so
+    // the persistent warps finish together (longest-processing-time order)
+    std::vector<uint32_t> weight(n_super, 0);
     uint32_t max_lsub = 0;
     double sum_lsub = 0.0;
     uint64_t n_sub_nonempty = 0;
@@ -287,6 +291,8 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
         uint32_t ml = 0;
         for (int j = 0; j < L.SD; ++j) {
             const uint32_t v = hsub[T * L.SD + j];
+            const uint32_t nb = (v + 7) / 8;
+            weight[T] += nb * (nb + 1) / 2;
             ml = std::max(ml, v);
             if (v) {
                 sum_lsub += v;
@@ -323,10 +329,18 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
         if (smax >= 0 && (int)assembly_min_smem(dim, kSuperCaps[lmax], kSubCaps[smax], L.SD) <= optin) {
             std::vector<uint32_t> all;
             for (auto& v : lists) all.insert(all.end(), v.begin(), v.end());
-            std::sort(all.begin(), all.end());
             for (auto& v : lists) v.clear();
             lists[smax * nlc + lmax] = std::move(all);
         }
+    }
+    const bool lpt = env_int("RBG_LPT", 1) != 0;
+    for (auto& v : lists) {
+        if (lpt)
+            std::sort(v.begin(), v.end(), [&](uint32_t a, uint32_t b) {
+                return weight[a] != weight[b] ? weight[a] > weight[b] : a < b;
+            });
+        else
+            std::sort(v.begin(), v.end());
     }
     L.buckets.clear();
     for (int si = 0; si < nsc; ++si)
