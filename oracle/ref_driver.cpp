@@ -14,7 +14,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <array>
+#include <optional>
+#include <span>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -291,6 +294,102 @@ int ref_evaluate_model_poly(const double* refs_xy, const double* w, const double
                     std::vector<double>(w, w + m), std::array<double, 3>{a[0], a[1], a[2]}, {0.0, 0.0}};
         const auto f = evaluate_model(model, to_points(q_xy, nq));
         std::memcpy(f_out, f.data(), nq * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// ---- on-disk formats: the reference's own writers/readers (model.cpp, data.cpp)
+// save_model (model.cpp:76-115); poly may be null.
+int ref_save_model(const char* path, int family, double alpha, const double* refs_xy, const double* w,
+                   std::uint64_t m, double offx, double offy, const double* poly) {
+    try {
+        std::optional<std::array<double, 3>> a;
+        if (poly) a = std::array<double, 3>{poly[0], poly[1], poly[2]};
+        Model model{KernelSpec(family_of(family), alpha), to_points(refs_xy, m), std::vector<double>(w, w + m), a,
+                    {offx, offy}};
+        save_model(model, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// load_model (model.cpp:117-190): scal = {alpha, offx, offy, poly[3]}; refs/w
+// sized by the caller (cap entries).
+int ref_load_model(const char* path, int* family, int* has_poly, std::uint64_t* m, double* scal,
+                   double* refs_xy, double* w, std::uint64_t cap) {
+    try {
+        const Model model = load_model(path);
+        *family = static_cast<int>(model.kernel.family());
+        *has_poly = model.poly ? 1 : 0;
+        *m = model.refs.size();
+        scal[0] = model.kernel.alpha();
+        scal[1] = model.offset.x;
+        scal[2] = model.offset.y;
+        for (int k = 0; k < 3; ++k) scal[3 + k] = model.poly ? (*model.poly)[k] : 0.0;
+        for (std::uint64_t j = 0; j < model.refs.size() && j < cap; ++j) {
+            refs_xy[2 * j] = model.refs[j].x;
+            refs_xy[2 * j + 1] = model.refs[j].y;
+            w[j] = model.weights[j];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// save_xyz (data.cpp:143-157)
+int ref_save_xyz(const char* path, const double* xy, const double* h, std::uint64_t n) {
+    try {
+        PointCloud c;
+        c.points = to_points(xy, n);
+        c.values.assign(h, h + n);
+        save_xyz(c, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// kind 0 load_xyz, 1 load_eval_points, 2 load_ref_points (data.cpp:126-196):
+// rows (n x arity) into out (cap doubles).
+int ref_load_records(const char* path, int kind, std::uint64_t* n, int* arity, double* out, std::uint64_t cap) {
+    try {
+        std::vector<double> rows;
+        if (kind == 0) {
+            const PointCloud c = load_xyz(path);
+            *arity = 3;
+            for (std::size_t i = 0; i < c.size(); ++i) rows.insert(rows.end(), {c.points[i].x, c.points[i].y, c.values[i]});
+        } else if (kind == 1) {
+            const EvalPoints e = load_eval_points(path);
+            *arity = e.has_values ? 3 : 2;
+            for (std::size_t i = 0; i < e.points.size(); ++i) {
+                rows.insert(rows.end(), {e.points[i].x, e.points[i].y});
+                if (e.has_values) rows.push_back(e.values[i]);
+            }
+        } else {
+            *arity = 2;
+            for (const Point2& p : load_ref_points(path)) rows.insert(rows.end(), {p.x, p.y});
+        }
+        *n = rows.size() / static_cast<std::uint64_t>(*arity);
+        std::memcpy(out, rows.data(), std::min<std::uint64_t>(cap, rows.size()) * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// write_signed_errors (model.cpp:234-256)
+int ref_write_signed_errors(const char* path, const double* xy, const double* h, std::uint64_t n, double offx,
+                            double offy, const double* pred) {
+    try {
+        PointCloud c;
+        c.points = to_points(xy, n);
+        c.values.assign(h, h + n);
+        c.offset = {offx, offy};
+        write_signed_errors(c, std::span<const double>(pred, n), path);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

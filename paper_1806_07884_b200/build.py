@@ -71,7 +71,7 @@ def build_rbg(force: bool = False, ptxas_verbose: bool = False) -> Path:
 
 
 def build_host(force: bool = False) -> Path:
-    srcs = [CSRC / "rbfit_gpu.cpp"]
+    srcs = [CSRC / "rbfit_gpu.cpp", CSRC / "rbfit_io.cpp"]
     deps = srcs + [CSRC / "rbfit_gpu.hpp", ROOT / "include" / "rbg.h", LIB_RBG]
     if force or _stale(LIB_HOST, deps):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", f"-I{ROOT / 'include'}",

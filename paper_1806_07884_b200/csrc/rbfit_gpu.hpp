@@ -18,6 +18,7 @@
 
 #include <array>
 #include <cstdint>
+#include <filesystem>
 #include <functional>
 #include <optional>
 #include <span>
@@ -180,5 +181,22 @@ struct ErrorReport {  // model.hpp:38-50 (+ rms, max)
 ErrorReport error_report(const Model& model, const PointCloud& cloud,
                          std::optional<std::size_t> design_nnz = std::nullopt,
                          Device* device = nullptr);
+
+// ---- on-disk formats (rbfit_io.cpp): byte-identical to the reference's files
+void save_model(const Model& model, const std::filesystem::path& path);  // model.cpp:76-115
+Model load_model(const std::filesystem::path& path);                     // model.cpp:117-190
+
+struct EvalPoints {  // data.hpp:49-53
+    std::vector<Point2> points;
+    std::vector<double> values;  // empty unless has_values
+    bool has_values = false;
+};
+PointCloud load_xyz(const std::filesystem::path& path);                      // data.cpp:126-141
+void save_xyz(const PointCloud& cloud, const std::filesystem::path& path);   // data.cpp:143-157
+EvalPoints load_eval_points(const std::filesystem::path& path);              // data.cpp:159-180
+std::vector<Point2> load_ref_points(const std::filesystem::path& path);      // data.cpp:182-196
+void write_signed_errors(const PointCloud& cloud, std::span<const double> predictions,
+                         const std::filesystem::path& path);                 // model.cpp:234-256
+PointCloud center_cloud(PointCloud cloud);                                   // data.cpp:198-223
 
 }  // namespace rbfit_b200

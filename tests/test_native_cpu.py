@@ -26,12 +26,24 @@ def test_every_declared_symbol_is_exported():
     assert set(syms) == set(_native.exported_symbols())
 
 
+def test_io_header_symbols_are_exported():
+    import ctypes
+
+    L = ctypes.CDLL(str(ROOT / "paper_1806_07884_b200" / "librbfit_b200.so"))
+    syms = sorted(set(re.findall(r"\b(rbfit_io_[a-z0-9_]+)\s*\(", (ROOT / "include" / "rbfit_io.h").read_text())))
+    assert len(syms) == 9
+    for s in syms:
+        assert hasattr(L, s), s
+
+
 def test_host_layer_library_exports_reference_api():
     import subprocess
     out = subprocess.run(["nm", "-DC", str(ROOT / "paper_1806_07884_b200" / "librbfit_b200.so")],
                          capture_output=True, text=True, check=True).stdout
     for name in ("rbfit_b200::fit(", "rbfit_b200::build_normal_system(", "rbfit_b200::solve_weights(",
-                 "rbfit_b200::evaluate_model(", "rbfit_b200::error_report(", "rbfit_b200::KernelSpec::evaluate"):
+                 "rbfit_b200::evaluate_model(", "rbfit_b200::error_report(", "rbfit_b200::KernelSpec::evaluate",
+                 "rbfit_b200::save_model(", "rbfit_b200::load_model(", "rbfit_b200::load_xyz(",
+                 "rbfit_b200::save_xyz(", "rbfit_b200::write_signed_errors(", "rbfit_b200::center_cloud("):
         assert name in out, name
 
 
