@@ -35,6 +35,7 @@ CU_SOURCES = (["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu"
 LIB_RBG = PKG / "librbg.so"
 LIB_HOST = PKG / "librbfit_b200.so"
 LIB_DATAGEN = PKG / "librbg_datagen.so"
+CLI = PKG / "rbfit-b200"
 
 
 def _run(cmd: list[str]) -> None:
@@ -88,6 +89,16 @@ def build_datagen(force: bool = False) -> Path:
     return LIB_DATAGEN
 
 
+def build_cli(force: bool = False) -> Path:
+    """rbfit-b200: the reference's gen-synthetic / fit / eval / bench-blocks front end."""
+    src = CSRC / "rbfit_b200_main.cpp"
+    deps = [src, CSRC / "rbfit_gpu.hpp", LIB_HOST, LIB_DATAGEN]
+    if force or _stale(CLI, deps):
+        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-o", str(CLI), str(src), f"-L{PKG}",
+              "-lrbfit_b200", "-lrbg", "-lrbg_datagen", "-Wl,-rpath,$ORIGIN"])
+    return CLI
+
+
 def build_oracle(force: bool = False) -> None:
     """CPU checkers (test infrastructure): our C restatement always; the
     reference's own sources only where /root/reference exists."""
@@ -105,6 +116,7 @@ def build_all(force: bool = False) -> None:
     build_rbg(force)
     build_host(force)
     build_datagen(force)
+    build_cli(force)
     build_oracle(force)
 
 

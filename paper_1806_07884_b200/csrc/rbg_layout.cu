@@ -169,7 +169,8 @@ int env_int(const char* name, int dflt) {
 // Sub-tile divisor q (sub edge = r/q) and super factor S from the point
 // density (measured on B200, profiles/): 2-D sub-tiles of about 34 points
 // (about nine 4-point DMMA k-steps per register pass), super-tiles of 2x2
-// sub-tiles, 3x3 once the sub-tiles are small (q >= 9); 3-D: sub-tiles of
+// sub-tiles, 3x3 from q >= 7 and 4x4 from q >= 9 (larger super-tiles amortise
+// the flush over more points until the accumulator costs occupancy); 3-D: sub-tiles of
 // edge r/2 assembled in direct mode (one sub-tile per super-tile, register
 // tiles reduced straight into the CSR values: a 3-D super-tile accumulator
 // would not fit shared memory).
@@ -182,7 +183,7 @@ static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* s
     if (dim == 2) {
         const double e = std::sqrt(34.0 / rho);
         q = std::max(2, std::min(16, (int)std::lround(r / e)));
-        S = q >= 9 ? 3 : 2;
+        S = q >= 9 ? 4 : q >= 7 ? 3 : 2;
     } else {
         q = 2;
         S = 1;

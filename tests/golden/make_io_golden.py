@@ -149,6 +149,13 @@ def main():
     out = cxy.copy()
     assert L.ref_center_cloud(out.ctypes.data, vals.ctypes.data, 1000, off.ctypes.data) == 0
     data.update(center_in=cxy, center_out=out, center_offset=off)
+    # `rbfit gen-synthetic -n 1089` (rbfit_main.cpp:120-125): make_franke_cloud + save_xyz
+    n = 1089
+    hal = np.empty(2 * n)
+    L.ref_halton_points(n, 2, hal.ctypes.data)
+    fr = np.array([L.ref_franke(hal[2 * i], hal[2 * i + 1]) for i in range(n)])
+    assert L.ref_save_xyz(bpath, hal.ctypes.data, fr.ctypes.data, n) == 0
+    data["gen1089_bytes"] = np.frombuffer(path.read_bytes(), dtype=np.uint8).copy()
     np.savez_compressed(OUT / "io_cases.npz", **data)
     print("io_cases.npz", (OUT / "io_cases.npz").stat().st_size)
 

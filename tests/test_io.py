@@ -110,3 +110,60 @@ def test_center_cloud_bitwise(g):
     xy, off = io.center_cloud(g["center_in"])
     assert np.array_equal(xy, g["center_out"])
     assert off == tuple(g["center_offset"]) or np.array_equal(np.array(off), g["center_offset"])
+
+
+# ---------------------------------------------------------------- CLI (§8(f) row 4)
+CLI = Path(__file__).resolve().parents[1] / "paper_1806_07884_b200" / "rbfit-b200"
+
+
+def _cli(*args):
+    import subprocess
+
+    return subprocess.run([str(CLI), *map(str, args)], capture_output=True, text=True)
+
+
+def test_cli_gen_synthetic_bytes_equal_reference(g, tmp_path):
+    out = tmp_path / "franke.xyz"
+    r = _cli("gen-synthetic", "-n", 1089, "--out", out)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout == "points 1089\n"
+    assert out.read_bytes() == bytes(g["gen1089_bytes"])
+
+
+def test_cli_usage_errors(tmp_path):
+    assert _cli().returncode == 106
+    assert _cli("frobnicate").returncode == 109
+    assert _cli("gen-synthetic", "-n", 5).returncode == 106  # --out required
+    assert _cli("gen-synthetic", "-n", "x", "--out", tmp_path / "a").returncode == 104
+    assert _cli("fit", "--in", "a", "--alpha", 1, "--model", "m").returncode == 1  # missing refs: error line
+    r = _cli("fit", "--in", tmp_path / "missing.xyz", "--alpha", 1, "--refs-grid", 4, "--model", tmp_path / "m")
+    assert r.returncode == 1 and r.stderr.startswith("error: cannot open")
+    r = _cli("fit", "--in", "a", "--alpha", 1, "--refs-grid", 4, "--refs-file", "b", "--model", "m")
+    assert r.returncode == 108
+    assert _cli("--help").returncode == 0
+
+
+@pytest.mark.gpu
+def test_cli_fit_and_eval_readme_case(golden, tmp_path):
+    """The README walk-through (proj/README.md:62-76) through the CLI: gen-synthetic,
+    fit on an 81-point grid with alpha 0.5, eval with values; the model file
+    loads back and the error lines agree between fit and eval."""
+    xyz, model = tmp_path / "franke.xyz", tmp_path / "model.txt"
+    assert _cli("gen-synthetic", "-n", 1089, "--out", xyz).returncode == 0
+    r = _cli("fit", "--in", xyz, "--kernel", "wendland-3-1", "--alpha", 0.5, "--refs-grid", 81, "--model", model)
+    assert r.returncode == 0, r.stderr
+    kv = dict(line.split(" ", 1) for line in r.stdout.strip().splitlines())
+    assert kv["points"] == "1089" and kv["refs"] == "81" and kv["design-nnz"] == "88209"
+    assert kv["n-blocks"] == "1" and kv["empty-support-refs"] == "0"
+    assert float(kv["mae"]) == pytest.approx(float(golden("readme_case")["published_mae"]), rel=1e-4)
+    assert "assembly:" in r.stderr
+    m = io.load_model(model)
+    assert len(m.refs) == 81 and m.kernel.alpha == 0.5
+    errs = tmp_path / "errors.txt"
+    r2 = _cli("eval", "--model", model, "--in", xyz, "--out", errs)
+    assert r2.returncode == 0, r2.stderr
+    kv2 = dict(line.split(" ", 1) for line in r2.stdout.strip().splitlines())
+    assert float(kv2["mae"]) == pytest.approx(float(kv["mae"]), rel=1e-12)
+    rows = np.loadtxt(errs)
+    assert rows.shape == (1089, 5)
+    np.testing.assert_allclose(rows[:, 4], rows[:, 3] - rows[:, 2], rtol=0, atol=1e-15)
