@@ -14,10 +14,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 cap() {  # cap NAME KERNEL_REGEX CONFIG
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o /tmp/${TAG}_$1 $CMD --config $3 > gpurun_out/${TAG}_ncu_$1.log 2>&1
   ncu -i /tmp/${TAG}_$1.ncu-rep --page raw --csv > gpurun_out/${TAG}_$1_raw.csv 2>/dev/null
+  ncu -i /tmp/${TAG}_$1.ncu-rep --page details --csv > gpurun_out/${TAG}_$1_details.csv 2>/dev/null
   ncu -i /tmp/${TAG}_$1.ncu-rep --page source --csv --print-source sass,cuda > /tmp/${TAG}_$1_src.csv 2>/dev/null
   python scripts/src_hot.py /tmp/${TAG}_$1_src.csv 40 > gpurun_out/${TAG}_$1_hot.txt 2>&1
   rm -f /tmp/${TAG}_$1.ncu-rep /tmp/${TAG}_$1_src.csv
 }
-for c in cfg2 cfg5 cfg4 cfg3 cfg1; do cap asm_$c assemble_warp $c; done
+for c in cfg2 cfg5 cfg4 cfg3; do cap asm_$c assemble_warp $c; done
 cap scatter_cfg5 bin_scatter cfg5
 echo done > gpurun_out/${TAG}_done.txt
