@@ -252,6 +252,7 @@ void setup_centres(rbg_ctx* ctx) {
     const int dim = ctx->dim;
     const uint64_t m = ctx->m;
     cudaStream_t st = ctx->stream;
+    ctx->bj_built = false;  // preconditioner blocks follow the centre set
 
     // ---- host: bounding box + tile grid plan ------------------------------
     std::vector<double> hc(m * dim);
