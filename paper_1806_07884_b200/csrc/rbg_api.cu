@@ -127,6 +127,7 @@ rbg_status rbg_destroy(rbg_ctx* ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& e : ctx->ev_asm)
         if (e) cudaEventDestroy(e);
+    rbg::release_staging(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return RBG_OK;
@@ -216,15 +217,17 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
     return guarded(ctx, [&] {
         require_centres(ctx);
         if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
-        if (validate) check_points_finite(points, n, ctx->dim, "non-finite coordinate at point index ");
         bind(ctx);
         if (n > 0) {
             ctx->in_pts.reserve(n * ctx->dim);
             ctx->in_h.reserve(n);
-            RBG_CUDA(cudaMemcpyAsync(ctx->in_pts.p, points, n * ctx->dim * sizeof(double),
-                                     cudaMemcpyHostToDevice, ctx->stream));
-            RBG_CUDA(cudaMemcpyAsync(ctx->in_h.p, h, n * sizeof(double), cudaMemcpyHostToDevice,
-                                     ctx->stream));
+            rbg::h2d(ctx, ctx->in_pts.p, points, n * ctx->dim * sizeof(double));
+            rbg::h2d(ctx, ctx->in_h.p, h, n * sizeof(double));
+            if (validate) {  // kdtree.cpp:14-17, checked on the device copy (first offending index)
+                const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, ctx->dim);
+                if (bad < n)
+                    throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
+            }
         }
         rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
     });
@@ -255,9 +258,7 @@ rbg_status rbg_get_system(rbg_ctx* ctx, double* values, double* rhs, double* hit
         check_misses(ctx);
         cudaStream_t st = ctx->stream;
         const uint64_t m = ctx->m;
-        if (values)
-            RBG_CUDA(cudaMemcpyAsync(values, ctx->sys.p, ctx->nnz_upper * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st));
+        if (values) rbg::d2h(ctx, values, ctx->sys.p, ctx->nnz_upper * sizeof(double));
         if (rhs)
             RBG_CUDA(cudaMemcpyAsync(rhs, ctx->sys.p + ctx->nnz_upper, m * sizeof(double),
                                      cudaMemcpyDeviceToHost, st));
@@ -319,7 +320,6 @@ rbg_status rbg_evaluate(rbg_ctx* ctx, const double* c, const double* q, uint64_t
     return guarded(ctx, [&] {
         require_centres(ctx);
         if (!c || (nq > 0 && (!q || !f))) throw Error(RBG_INVALID_ARGUMENT, "null array");
-        check_points_finite(q, nq, ctx->dim, "evaluate_model: non-finite query point at index ");
         bind(ctx);
         cudaStream_t st = ctx->stream;
         ctx->ev_c.reserve(ctx->m);
@@ -327,11 +327,11 @@ rbg_status rbg_evaluate(rbg_ctx* ctx, const double* c, const double* q, uint64_t
         if (nq == 0) return;
         ctx->ev_q.reserve(nq * ctx->dim);
         ctx->ev_f.reserve(nq);
-        RBG_CUDA(cudaMemcpyAsync(ctx->ev_q.p, q, nq * ctx->dim * sizeof(double),
-                                 cudaMemcpyHostToDevice, st));
+        rbg::h2d(ctx, ctx->ev_q.p, q, nq * ctx->dim * sizeof(double));
+        if (const uint64_t bad = rbg::first_nonfinite(ctx, ctx->ev_q.p, nq, ctx->dim); bad < nq)  // model.cpp:60
+            throw Error(RBG_INVALID_ARGUMENT, "evaluate_model: non-finite query point at index " + std::to_string(bad));
         rbg::evaluate_points(ctx, ctx->ev_c.p, ctx->ev_q.p, nq, ctx->ev_f.p);
-        RBG_CUDA(cudaMemcpyAsync(f, ctx->ev_f.p, nq * sizeof(double), cudaMemcpyDeviceToHost, st));
-        RBG_CUDA(cudaStreamSynchronize(st));
+        rbg::d2h(ctx, f, ctx->ev_f.p, nq * sizeof(double));
     });
 }
 
@@ -348,15 +348,12 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
         ctx->ev_f.reserve(n);
         ctx->ev_h.reserve(n);
         RBG_CUDA(cudaMemcpyAsync(ctx->ev_c.p, c, ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
-        RBG_CUDA(cudaMemcpyAsync(ctx->ev_q.p, points, n * ctx->dim * sizeof(double),
-                                 cudaMemcpyHostToDevice, st));
-        RBG_CUDA(cudaMemcpyAsync(ctx->ev_h.p, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        rbg::h2d(ctx, ctx->ev_q.p, points, n * ctx->dim * sizeof(double));
+        rbg::h2d(ctx, ctx->ev_h.p, h, n * sizeof(double));
         rbg::evaluate_points(ctx, ctx->ev_c.p, ctx->ev_q.p, n, ctx->ev_f.p);
         rbg::error_stats(ctx, ctx->ev_f.p, ctx->ev_h.p, n, out);
         if (signed_errors) {
-            RBG_CUDA(cudaMemcpyAsync(signed_errors, ctx->ev_f.p, n * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st));
-            RBG_CUDA(cudaStreamSynchronize(st));
+            rbg::d2h(ctx, signed_errors, ctx->ev_f.p, n * sizeof(double));
             for (uint64_t i = 0; i < n; ++i) signed_errors[i] = signed_errors[i] - h[i];  // model.cpp:208
         }
     });

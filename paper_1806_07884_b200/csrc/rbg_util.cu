@@ -1,5 +1,10 @@
 // rbg_util.cu -- exclusive scans and a warp-per-segment bitonic sort used by
 // the binning (counting sort) and symbolic (pattern) phases.
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include <vector>
+
 #include "rbg_internal.cuh"
 
 namespace rbg {
@@ -171,6 +176,122 @@ void segmented_sort_u32(rbg_ctx* ctx, uint32_t* keys, const uint64_t* seg_ptr, u
     segsort_warp<<<(unsigned)(blocks > 148u * 128u ? 148u * 128u : blocks), warps * 32, smem,
                    ctx->stream>>>(keys, seg_ptr, n_segs, p2);
     RBG_CHECK_LAUNCH(ctx);
+}
+
+
+// ------------------------------------------------------- staged host copies
+namespace {
+
+constexpr size_t kStageBytes = size_t{64} << 20;
+constexpr size_t kDirectBytes = size_t{16} << 20;
+
+bool page_locked(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void ensure_staging(rbg_ctx* ctx) {
+    for (int b = 0; b < 2; ++b) {
+        if (!ctx->pin[b]) RBG_CUDA(cudaHostAlloc(&ctx->pin[b], kStageBytes, cudaHostAllocPortable));
+        if (!ctx->pin_ev[b]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->pin_ev[b], cudaEventDisableTiming));
+    }
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const size_t per = (bytes + hw - 1) / hw;
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < hw && t * per < bytes; ++t)
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + t * per, static_cast<const char*>(src) + t * per,
+                        std::min(per, bytes - t * per));
+        });
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+void h2d(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    cudaStream_t st = ctx->stream;
+    if (bytes < kDirectBytes || page_locked(src)) {
+        RBG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    ensure_staging(ctx);
+    size_t off = 0;
+    for (int i = 0; off < bytes; ++i) {
+        const int b = i & 1;
+        const size_t len = std::min(kStageBytes, bytes - off);
+        RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[b]));  // the copy that last read this buffer is done
+        parallel_memcpy(ctx->pin[b], static_cast<const char*>(src) + off, len);
+        RBG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->pin[b], len, cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaEventRecord(ctx->pin_ev[b], st));
+        off += len;
+    }
+    RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[0]));
+    RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[1]));
+}
+
+void d2h(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    cudaStream_t st = ctx->stream;
+    if (bytes < kDirectBytes || page_locked(dst)) {
+        RBG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    ensure_staging(ctx);
+    const size_t n_chunks = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](size_t i) {
+        const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
+        RBG_CUDA(cudaMemcpyAsync(ctx->pin[i & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaEventRecord(ctx->pin_ev[i & 1], st));
+    };
+    issue(0);
+    for (size_t i = 0; i < n_chunks; ++i) {
+        RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[i & 1]));
+        if (i + 1 < n_chunks) issue(i + 1);  // the next chunk lands while this one drains
+        const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
+        parallel_memcpy(static_cast<char*>(dst) + off, ctx->pin[i & 1], len);
+    }
+}
+
+void release_staging(rbg_ctx* ctx) {
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
+        if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
+        ctx->pin[b] = nullptr;
+        ctx->pin_ev[b] = nullptr;
+    }
+}
+
+namespace {
+__global__ void first_nonfinite_kernel(const double* __restrict__ p, uint64_t n, int dim,
+                                       unsigned long long* __restrict__ first) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        bool ok = true;
+        for (int d = 0; d < dim; ++d) ok = ok && isfinite(p[i * dim + d]);
+        if (!ok) atomicMin(first, (unsigned long long)i);
+    }
+}
+}  // namespace
+
+uint64_t first_nonfinite(rbg_ctx* ctx, const double* d_pts, uint64_t n, int dim) {
+    if (n == 0) return 0;
+    cudaStream_t st = ctx->stream;
+    unsigned long long* slot = ctx->counters.p + 1;  // [1] scratch
+    const unsigned long long init = n;
+    RBG_CUDA(cudaMemcpyAsync(slot, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    first_nonfinite_kernel<<<blocks_for(n, 256), 256, 0, st>>>(d_pts, n, dim, slot);
+    RBG_CHECK_LAUNCH(ctx);
+    unsigned long long first = n;
+    RBG_CUDA(cudaMemcpyAsync(&first, slot, sizeof(first), cudaMemcpyDeviceToHost, st));
+    RBG_CUDA(cudaStreamSynchronize(st));
+    return first;
 }
 
 }  // namespace rbg
