@@ -128,6 +128,9 @@ rbg_status rbg_destroy(rbg_ctx* ctx) {
     for (auto& e : ctx->ev_asm)
         if (e) cudaEventDestroy(e);
     rbg::release_staging(ctx);
+    for (auto& e : ctx->chunk_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     return RBG_OK;
@@ -218,18 +221,65 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
         require_centres(ctx);
         if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
         bind(ctx);
+        const int dim = ctx->dim;
+        // Pinned inputs of a million points or more are uploaded in chunks on a
+        // copy stream, each chunk assembled (accumulating) as soon as it has
+        // landed, so the upload overlaps the binning and assembly of the chunks
+        // before it.  Pageable inputs go through the staging ring in one piece.
+        static const int chunks_env = [] {
+            const char* e = std::getenv("RBG_H2D_CHUNKS");
+            return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
+        }();
+        int K = 1;
+        if (n >= 1000000 && rbg::page_locked(points) && rbg::page_locked(h))
+            K = chunks_env ? chunks_env : (n >= 4000000 ? 4 : 2);
         if (n > 0) {
-            ctx->in_pts.reserve(n * ctx->dim);
+            ctx->in_pts.reserve(n * dim);
             ctx->in_h.reserve(n);
-            rbg::h2d(ctx, ctx->in_pts.p, points, n * ctx->dim * sizeof(double));
-            rbg::h2d(ctx, ctx->in_h.p, h, n * sizeof(double));
-            if (validate) {  // kdtree.cpp:14-17, checked on the device copy (first offending index)
-                const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, ctx->dim);
-                if (bad < n)
-                    throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
-            }
         }
-        rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
+        if (K == 1) {
+            if (n > 0) {
+                rbg::h2d(ctx, ctx->in_pts.p, points, n * dim * sizeof(double));
+                rbg::h2d(ctx, ctx->in_h.p, h, n * sizeof(double));
+                if (validate) {  // kdtree.cpp:14-17, checked on the device copy (first offending index)
+                    const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, dim);
+                    if (bad < n)
+                        throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
+                }
+            }
+            rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
+            return;
+        }
+        if (!ctx->lay.built) rbg::build_layout(ctx, n);  // tile sizes follow the whole batch's density
+        if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int c = 0; c < K; ++c)
+            if (!ctx->chunk_ev[c]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[c], cudaEventDisableTiming));
+        // the copy stream must not overwrite inputs a previous call is still reading
+        RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->stream));
+        RBG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
+        std::vector<uint64_t> off(K + 1);
+        for (int c = 0; c <= K; ++c) off[c] = n * (uint64_t)c / (uint64_t)K;
+        for (int c = 0; c < K; ++c) {
+            const uint64_t a = off[c], len = off[c + 1] - a;
+            RBG_CUDA(cudaMemcpyAsync(ctx->in_pts.p + a * dim, points + a * dim, len * dim * sizeof(double),
+                                     cudaMemcpyHostToDevice, ctx->copy_stream));
+            RBG_CUDA(cudaMemcpyAsync(ctx->in_h.p + a, h + a, len * sizeof(double), cudaMemcpyHostToDevice,
+                                     ctx->copy_stream));
+            RBG_CUDA(cudaEventRecord(ctx->chunk_ev[c], ctx->copy_stream));
+        }
+        for (int c = 0; c < K; ++c) {
+            const uint64_t a = off[c], len = off[c + 1] - a;
+            RBG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[c], 0));
+            if (validate) {
+                const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p + a * dim, len, dim);
+                if (bad < len) {
+                    RBG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+                    ctx->have_system = false;
+                    throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(a + bad));
+                }
+            }
+            rbg::assemble_points(ctx, ctx->in_pts.p + a * dim, ctx->in_h.p + a, len, accumulate != 0 || c > 0);
+        }
     });
 }
 

@@ -185,6 +185,8 @@ namespace {
 constexpr size_t kStageBytes = size_t{64} << 20;
 constexpr size_t kDirectBytes = size_t{16} << 20;
 
+}  // namespace
+
 bool page_locked(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -193,6 +195,8 @@ bool page_locked(const void* p) {
     }
     return a.type == cudaMemoryTypeHost;
 }
+
+namespace {
 
 void ensure_staging(rbg_ctx* ctx) {
     for (int b = 0; b < 2; ++b) {
