@@ -359,3 +359,48 @@ def test_border_slab_allreduce_sum(eng):
         _border_close(one, po.border(pts, h, refs, 1, 6.0))
     finally:
         eng.set_poly(False)
+
+
+_SUBPROC = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import pyoracle as po
+from paper_1806_07884_b200 import api, configs
+cfg = configs.CONFIGS["cfg2"]
+xy, h = configs.points("cfg2", n=1_200_000)
+refs = configs.centres("cfg2")
+k = api.KernelSpec(cfg.kernel, cfg.alpha)
+with api.Engine(0) as eng:
+    eng.set_centres(refs, k)
+    pxy, ph = torch.from_numpy(xy).pin_memory(), torch.from_numpy(h).pin_memory()
+    eng.assemble_ptr(pxy.data_ptr(), ph.data_ptr(), len(h), validate=True)
+    s = eng.system()
+    c, d = eng.solve()
+rp, cols = po.pattern(refs, cfg.alpha)
+ov, orhs, ohits = po.assemble(xy, h, refs, k.family, cfg.alpha, rp, cols)
+den = np.max(np.abs(ov))
+print("sys", np.max(np.abs(s["values"] - ov)) / den, np.max(np.abs(s["rhs"] - orhs)) / np.max(np.abs(orhs)),
+      int(np.array_equal(s["hits"].astype(np.uint64), ohits)))
+oc, _ = po.pcg(rp, cols, ov, orhs, tol=1e-12)
+print("c", np.max(np.abs(c - oc)) / np.max(np.abs(oc)), d["iterations"])
+"""
+
+
+@pytest.mark.parametrize("env", [{"RBG_H2D_CHUNKS": "3"}, {"RBG_PREC": "jacobi"}])
+def test_chunked_upload_and_point_jacobi_paths(env):
+    """The chunked pinned-upload path of rbg_assemble (accumulating chunks) and
+    the point-Jacobi PCG (RBG_PREC=jacobi) against the oracle, cfg2 geometry at
+    1.2e6 points (both knobs are read once per process, hence a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _SUBPROC.format(root=root)], capture_output=True, text=True,
+                       env={**os.environ, **env}, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = dict(l.split(" ", 1) for l in r.stdout.strip().splitlines() if l.startswith(("sys", "c ")))
+    eb, er, hits = lines["sys"].split()
+    assert float(eb) < TOL_SYS and float(er) < TOL_SYS and hits == "1"
+    assert float(lines["c"].split()[0]) < TOL_C
