@@ -188,10 +188,24 @@ __global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_
     double v[1] = {0.0};
     for (uint64_t row = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < m;
          row += warps) {
-        double s = 0.0;
+        // four independent 32-entry chunks in flight per lane (memory-level
+        // parallelism: a row is ~100-200 entries); the matrix streams past L2
+        // (evict-first) so the gathered vector p stays resident
         const uint64_t e1 = fptr[row + 1];
-        for (uint64_t e = fptr[row] + lane; e < e1; e += 32) s = fma(vfull[e], p[fcols[e]], s);
-        s = warp_sum(s);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        uint64_t e = fptr[row] + lane;
+        for (; e + 96 < e1; e += 128) {
+            const uint32_t c0 = __ldcs(fcols + e), c1 = __ldcs(fcols + e + 32), c2 = __ldcs(fcols + e + 64),
+                           c3 = __ldcs(fcols + e + 96);
+            const double v0 = __ldcs(vfull + e), v1 = __ldcs(vfull + e + 32), v2 = __ldcs(vfull + e + 64),
+                         v3 = __ldcs(vfull + e + 96);
+            s0 = fma(v0, p[c0], s0);
+            s1 = fma(v1, p[c1], s1);
+            s2 = fma(v2, p[c2], s2);
+            s3 = fma(v3, p[c3], s3);
+        }
+        for (; e < e1; e += 32) s0 = fma(__ldcs(vfull + e), p[__ldcs(fcols + e)], s0);
+        double s = warp_sum((s0 + s1) + (s2 + s3));
         if (lane == 0) {
             for (int t = 0; t < bd.T; ++t) s = fma(bd.E[(uint64_t)t * m + row], p[m + t], s);
             const double pi = p[row];
@@ -429,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) bj_update_kernel(uint64_t m, uint64_
         uint32_t i = 0;
         double ri = 0.0;
         if (k < m) {
-            i = perm[k];
+            i = perm ? perm[k] : (uint32_t)k;  // null: the solve runs in Morton order
             if (INIT) {
                 ri = r[i];
             } else {
@@ -470,6 +484,44 @@ __global__ void __launch_bounds__(kThreads) bj_update_kernel(uint64_t m, uint64_
     }
 }
 
+// Full CSR in Morton order: new row k = centre perm[k], columns renumbered by
+// pos (unsorted within the row: the SpMV does not need it), f2u carried along.
+__global__ void perm_len_kernel(const uint64_t* __restrict__ fptr, const uint64_t* __restrict__ uptr,
+                                const uint32_t* __restrict__ perm, uint64_t m, uint32_t* __restrict__ len,
+                                uint64_t* __restrict__ puptr) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = perm[k];
+        len[k] = (uint32_t)(fptr[i + 1] - fptr[i]);
+        puptr[k] = uptr[i];
+    }
+}
+
+__global__ void perm_fill_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
+                                 const uint64_t* __restrict__ f2u, const uint32_t* __restrict__ perm,
+                                 const uint32_t* __restrict__ pos, uint64_t m, const uint64_t* __restrict__ pfptr,
+                                 uint32_t* __restrict__ pfcols, uint64_t* __restrict__ pf2u) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t k = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5); k < m; k += warps) {
+        const uint32_t i = perm[k];
+        const uint64_t s0 = fptr[i], n = fptr[i + 1] - s0, d0 = pfptr[k];
+        for (uint64_t e = lane; e < n; e += 32) {
+            pfcols[d0 + e] = pos[fcols[s0 + e]];
+            pf2u[d0 + e] = f2u[s0 + e];
+        }
+    }
+}
+
+// v_out[k] = v[perm[k]] (to Morton order) or v_out[perm[k]] = v[k] (back).
+template <bool TO_MORTON>
+__global__ void permute_kernel(const uint32_t* __restrict__ perm, uint64_t m, const double* __restrict__ v,
+                               double* __restrict__ out) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+        if (TO_MORTON) out[k] = v[perm[k]];
+        else out[perm[k]] = v[k];
+    }
+}
+
 // Morton permutation of the centres and its inverse (once per centre set).
 void bj_build_order(rbg_ctx* ctx) {
     const uint64_t m = ctx->m;
@@ -498,6 +550,23 @@ void bj_build_order(rbg_ctx* ctx) {
     RBG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end
     ctx->bj_nblk = (m + kBJ - 1) / kBJ;
     ctx->bj_inv.reserve(ctx->bj_nblk * kBJ * kBJ);
+    {
+        DevBuf<uint32_t> len;
+        len.reserve(m + 1);
+        ctx->pfptr.reserve(m + 1);
+        ctx->puptr.reserve(m);
+        ctx->pfcols.reserve(ctx->nnz_full);
+        ctx->pf2u.reserve(ctx->nnz_full);
+        perm_len_kernel<<<blocks_for(m, 256), 256, 0, st>>>(ctx->fptr.p, ctx->uptr.p, ctx->bj_perm.p, m, len.p,
+                                                           ctx->puptr.p);
+        RBG_CHECK_LAUNCH(ctx);
+        exclusive_scan_u32_to_u64(ctx, len.p, ctx->pfptr.p, m);
+        perm_fill_kernel<<<blocks_for(m, 8, 148u * 16u), 256, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->f2u.p,
+                                                                      ctx->bj_perm.p, ctx->bj_pos.p, m, ctx->pfptr.p,
+                                                                      ctx->pfcols.p, ctx->pf2u.p);
+        RBG_CHECK_LAUNCH(ctx);
+        RBG_CUDA(cudaStreamSynchronize(st));
+    }
     ctx->bj_built = true;
 }
 
@@ -536,10 +605,28 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     RBG_CUDA(cudaMemsetAsync(ctx->ticket.p, 0, sizeof(unsigned), st));
     RBG_CUDA(cudaMemsetAsync(ctx->scal.p, 0, S_COUNT * sizeof(double), st));
 
+    // preconditioner: block Jacobi unless RBG_PREC=jacobi or the system is bordered;
+    // the block-Jacobi solve runs in the Morton order of its blocks
+    static const bool bj_env = [] {
+        const char* e = std::getenv("RBG_PREC");
+        return !(e && std::string(e) == "jacobi");
+    }();
+    const bool use_bj = bj_env && T == 0;
+    if (use_bj && !ctx->bj_built) bj_build_order(ctx);
+    const uint64_t* s_fptr = use_bj ? ctx->pfptr.p : ctx->fptr.p;
+    const uint32_t* s_fcols = use_bj ? ctx->pfcols.p : ctx->fcols.p;
+    const uint64_t* s_uptr = use_bj ? ctx->puptr.p : ctx->uptr.p;  // diagonal of each solve row
+
     RBG_CUDA(cudaEventRecord(ctx->ev0, st));
-    gather_full_kernel<<<blocks_for(nnz, kThreads), kThreads, 0, st>>>(ctx->f2u.p, uvals, nnz,
-                                                                        ctx->vfull.p);
+    gather_full_kernel<<<blocks_for(nnz, kThreads), kThreads, 0, st>>>(use_bj ? ctx->pf2u.p : ctx->f2u.p, uvals,
+                                                                        nnz, ctx->vfull.p);
     RBG_CHECK_LAUNCH(ctx);
+    if (use_bj) {  // right-hand side to Morton order
+        ctx->bvec.reserve(m);
+        permute_kernel<true><<<g_vec, kThreads, 0, st>>>(ctx->bj_perm.p, m, b, ctx->bvec.p);
+        RBG_CHECK_LAUNCH(ctx);
+        b = ctx->bvec.p;
+    }
     trace_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, m, ctx->partials.p, ctx->ticket.p,
                                              ctx->scal.p);
     RBG_CHECK_LAUNCH(ctx);
@@ -549,13 +636,6 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     for (int t = 0; t < T; ++t) trace += hF[t * T + t];
     const double mean_diag = trace / (double)nt;  // solver.cpp:296 (trace / side)
 
-    // preconditioner: block Jacobi unless RBG_PREC=jacobi or the system is bordered
-    static const bool bj_env = [] {
-        const char* e = std::getenv("RBG_PREC");
-        return !(e && std::string(e) == "jacobi");
-    }();
-    const bool use_bj = bj_env && T == 0;
-    if (use_bj && !ctx->bj_built) bj_build_order(ctx);
     const unsigned g_bj = use_bj ? blocks_for(ctx->bj_nblk, kThreads / 32, 148u * 8u) : 0u;
     if (use_bj) ctx->partials.reserve(std::max<uint64_t>(4ull * g_max, 4ull * g_bj));
 
@@ -567,11 +647,11 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
         if (T)
             border_dot_kernel<<<g_vec, kThreads, 0, st>>>(bd, ctx->p.p, ctx->partials.p, ctx->ticket.p,
                                                           ctx->scal.p, 0);
-        spmv_dot_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, bd,
+        spmv_dot_kernel<<<g_spmv, kThreads, 0, st>>>(s_fptr, s_fcols, ctx->vfull.p, m, bd,
                                                      ctx->p.p, ctx->q.p, ctx->partials.p,
                                                      ctx->ticket.p, ctx->scal.p);
         if (use_bj)
-            bj_update_kernel<false><<<g_bj, kThreads, 0, st>>>(m, ctx->bj_nblk, ctx->bj_perm.p, ctx->bj_inv.p,
+            bj_update_kernel<false><<<g_bj, kThreads, 0, st>>>(m, ctx->bj_nblk, nullptr, ctx->bj_inv.p,
                                                                ctx->q.p, ctx->x.p, ctx->r.p, ctx->z.p, ctx->p.p,
                                                                ctx->partials.p, ctx->ticket.p, ctx->scal.p);
         else
@@ -596,7 +676,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                                      cudaMemcpyHostToDevice, st));
             RBG_CUDA(cudaMemcpyAsync(ctx->scal.p + S_MAXIT, &init[1], sizeof(double),
                                      cudaMemcpyHostToDevice, st));
-            init_kernel<<<g_vec, kThreads, 0, st>>>(ctx->uptr.p, uvals, b, m, bd, ctx->dinv.p, ctx->x.p,
+            init_kernel<<<g_vec, kThreads, 0, st>>>(s_uptr, uvals, b, m, bd, ctx->dinv.p, ctx->x.p,
                                                     ctx->r.p, ctx->z.p, ctx->p.p, ctx->partials.p,
                                                     ctx->ticket.p, ctx->scal.p, tol * tol);
             RBG_CHECK_LAUNCH(ctx);
@@ -605,7 +685,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                                                                         ctx->bj_perm.p, ctx->bj_pos.p, ctx->scal.p,
                                                                         ctx->bj_inv.p);
                 RBG_CHECK_LAUNCH(ctx);
-                bj_update_kernel<true><<<g_bj, kThreads, 0, st>>>(m, ctx->bj_nblk, ctx->bj_perm.p, ctx->bj_inv.p,
+                bj_update_kernel<true><<<g_bj, kThreads, 0, st>>>(m, ctx->bj_nblk, nullptr, ctx->bj_inv.p,
                                                                   ctx->q.p, ctx->x.p, ctx->r.p, ctx->z.p, ctx->p.p,
                                                                   ctx->partials.p, ctx->ticket.p, ctx->scal.p);
                 RBG_CHECK_LAUNCH(ctx);
@@ -640,7 +720,15 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
         RBG_CUDA(cudaMemcpyAsync(dg.data(), ctx->dinv.p, nt * sizeof(double), cudaMemcpyDeviceToHost, st));
         RBG_CUDA(cudaStreamSynchronize(st));
         uint64_t piv = 0;
-        while (piv < nt && dg[piv] > 0.0 && std::isfinite(dg[piv])) ++piv;
+        if (use_bj) {  // solve rows are in Morton order: the first bad centre id
+            std::vector<uint32_t> perm(m);
+            RBG_CUDA(cudaMemcpy(perm.data(), ctx->bj_perm.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            piv = nt;
+            for (uint64_t k = 0; k < m; ++k)
+                if (!(dg[k] > 0.0 && std::isfinite(dg[k]))) piv = std::min<uint64_t>(piv, perm[k]);
+        } else {
+            while (piv < nt && dg[piv] > 0.0 && std::isfinite(dg[piv])) ++piv;
+        }
         if (piv == nt) piv = 0;
         throw Error(RBG_RUNTIME_ERROR,
                     "normal system is not positive definite even with ridge 1e-06; first "
@@ -651,9 +739,14 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                                                       ctx->scal.p, 1);
         RBG_CHECK_LAUNCH(ctx);
     }
-    residual_kernel<<<g_spmv, kThreads, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->vfull.p, m, bd, ctx->x.p,
+    residual_kernel<<<g_spmv, kThreads, 0, st>>>(s_fptr, s_fcols, ctx->vfull.p, m, bd, ctx->x.p,
                                                  b, ctx->partials.p, ctx->ticket.p, ctx->scal.p);
     RBG_CHECK_LAUNCH(ctx);
+    if (use_bj) {  // solution back to centre order (x stays in centre order for its readers)
+        permute_kernel<false><<<g_vec, kThreads, 0, st>>>(ctx->bj_perm.p, m, ctx->x.p, ctx->q.p);
+        RBG_CHECK_LAUNCH(ctx);
+        RBG_CUDA(cudaMemcpyAsync(ctx->x.p, ctx->q.p, m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
     RBG_CUDA(cudaEventRecord(ctx->ev1, st));
     double rr_true = 0.0, bb = 0.0;
     RBG_CUDA(cudaMemcpyAsync(&rr_true, ctx->scal.p + S_PQ, sizeof(double), cudaMemcpyDeviceToHost, st));
