@@ -522,6 +522,16 @@ __global__ void permute_kernel(const uint32_t* __restrict__ perm, uint64_t m, co
     }
 }
 
+// Grid of a grid-stride kernel: at most one full wave of resident CTAs (a
+// partial second wave leaves SMs idle at the tail of every launch).
+template <typename K>
+unsigned resident_grid(rbg_ctx* ctx, K kern, unsigned needed) {
+    int per_sm = 0, sms = 0;
+    RBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+    RBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    return std::max(1u, std::min(needed, (unsigned)std::max(1, per_sm * sms)));
+}
+
 // Morton permutation of the centres and its inverse (once per centre set).
 void bj_build_order(rbg_ctx* ctx) {
     const uint64_t m = ctx->m;
@@ -597,7 +607,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     ctx->vfull.reserve(nnz);
     for (auto* v : {&ctx->x, &ctx->r, &ctx->z, &ctx->p, &ctx->q, &ctx->dinv}) v->reserve(nt);
     const unsigned g_vec = blocks_for(nt, kThreads, 148u * 4u);
-    const unsigned g_spmv = blocks_for(m, kThreads / 32, 148u * 8u);
+    const unsigned g_spmv = resident_grid(ctx, spmv_dot_kernel, blocks_for(m, kThreads / 32, ~0u));
     const unsigned g_max = std::max(g_vec, g_spmv);
     ctx->partials.reserve(4ull * g_max);
     ctx->scal.reserve(S_COUNT);
@@ -636,7 +646,8 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     for (int t = 0; t < T; ++t) trace += hF[t * T + t];
     const double mean_diag = trace / (double)nt;  // solver.cpp:296 (trace / side)
 
-    const unsigned g_bj = use_bj ? blocks_for(ctx->bj_nblk, kThreads / 32, 148u * 8u) : 0u;
+    const unsigned g_bj =
+        use_bj ? resident_grid(ctx, bj_update_kernel<false>, blocks_for(ctx->bj_nblk, kThreads / 32, ~0u)) : 0u;
     if (use_bj) ctx->partials.reserve(std::max<uint64_t>(4ull * g_max, 4ull * g_bj));
 
     // one batch of iterations as a graph (kernels read their scalars on device)
