@@ -176,8 +176,14 @@ __global__ void border_dot_kernel(BorderDev bd, const double* __restrict__ v, do
         for (int t = 0; t < 4; ++t) scal[S_W0 + t] = out[t];
 }
 
+// six resident CTAs per SM (40 registers, no spills): 48 warps of row streams
+// instead of 40 (cfg5 solve 378 -> 351 ms, cfg4 285 -> 269 ms)
+#ifndef RBG_SPMV_MINB
+#define RBG_SPMV_MINB 6
+#endif
+#define RBG_SPMV_BOUNDS __launch_bounds__(kThreads, RBG_SPMV_MINB)
 // q = (B + shift I) p, one warp per row; pq = p.q.
-__global__ void spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
+__global__ void RBG_SPMV_BOUNDS spmv_dot_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
                                 const double* __restrict__ vfull, uint64_t m, BorderDev bd,
                                 const double* __restrict__ p, double* __restrict__ q,
                                 double* partials, unsigned* ticket, double* scal) {
