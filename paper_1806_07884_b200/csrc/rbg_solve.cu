@@ -318,7 +318,12 @@ __global__ void residual_kernel(const uint64_t* __restrict__ fptr, const uint32_
 // against point Jacobi for one extra kBJ^2 matvec per iteration.  A
 // non-positive pivot in a block flags the attempt as failed, so the
 // reference's ridge ladder (solver.cpp:296-315) moves to the next lambda.
-constexpr int kBJ = 32;  // one warp per block in the apply
+#ifndef RBG_BJ
+#define RBG_BJ 32
+#endif
+constexpr int kBJ = RBG_BJ;      // block size (a multiple of 32): one warp per block in the apply
+constexpr int kRPL = kBJ / 32;   // block rows per lane in the apply
+static_assert(kBJ % 32 == 0, "block-Jacobi block size must be a multiple of 32");
 
 __device__ __forceinline__ uint64_t spread_bits(uint64_t v, int dim) {
     if (dim == 2) {  // 32 -> 64 bits
@@ -368,8 +373,9 @@ __global__ void __launch_bounds__(kBJ) bj_setup_kernel(const uint64_t* __restric
                                                        const uint32_t* __restrict__ perm,
                                                        const uint32_t* __restrict__ pos, double* scal,
                                                        double* __restrict__ inv) {
-    __shared__ double D[kBJ][kBJ + 1];
-    __shared__ double Li[kBJ][kBJ + 1];
+    extern __shared__ double bj_sm[];  // D and Li, kBJ x (kBJ + 1) each
+    double (*D)[kBJ + 1] = reinterpret_cast<double (*)[kBJ + 1]>(bj_sm);
+    double (*Li)[kBJ + 1] = reinterpret_cast<double (*)[kBJ + 1]>(bj_sm + kBJ * (kBJ + 1));
     __shared__ int bad;
     const uint64_t b = blockIdx.x;
     const int t = threadIdx.x;
@@ -445,31 +451,46 @@ __global__ void __launch_bounds__(kThreads) bj_update_kernel(uint64_t m, uint64_
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double v[2] = {0.0, 0.0};
     for (uint64_t b = blockIdx.x * (uint64_t)(kThreads / 32) + w; b < nblk; b += (uint64_t)gridDim.x * (kThreads / 32)) {
-        const uint64_t k = b * kBJ + lane;
-        uint32_t i = 0;
-        double ri = 0.0;
-        if (k < m) {
-            i = perm ? perm[k] : (uint32_t)k;  // null: the solve runs in Morton order
-            if (INIT) {
-                ri = r[i];
-            } else {
-                x[i] += a * p[i];
-                ri = r[i] - a * q[i];
-                r[i] = ri;
+        uint32_t i[kRPL];
+        double ri[kRPL];
+#pragma unroll
+        for (int u = 0; u < kRPL; ++u) {
+            const uint64_t k = b * kBJ + u * 32 + lane;
+            i[u] = 0;
+            ri[u] = 0.0;
+            if (k < m) {
+                i[u] = perm ? perm[k] : (uint32_t)k;  // null: the solve runs in Morton order
+                if (INIT) {
+                    ri[u] = r[i[u]];
+                } else {
+                    x[i[u]] += a * p[i[u]];
+                    ri[u] = r[i[u]] - a * q[i[u]];
+                    r[i[u]] = ri[u];
+                }
             }
+            rs[w][u * 32 + lane] = ri[u];
         }
-        rs[w][lane] = ri;
         __syncwarp();
         const double* Bi = inv + b * (uint64_t)(kBJ * kBJ);
-        double zi = 0.0;
+        double zi[kRPL];
+#pragma unroll
+        for (int u = 0; u < kRPL; ++u) zi[u] = 0.0;
 #pragma unroll 8
-        for (int j = 0; j < kBJ; ++j) zi = fma(__ldg(Bi + j * kBJ + lane), rs[w][j], zi);
+        for (int j = 0; j < kBJ; ++j) {
+            const double rj = rs[w][j];
+#pragma unroll
+            for (int u = 0; u < kRPL; ++u) zi[u] = fma(__ldg(Bi + j * kBJ + u * 32 + lane), rj, zi[u]);
+        }
         __syncwarp();
-        if (k < m) {
-            z[i] = zi;
-            if (INIT) p[i] = zi;
-            v[0] += ri * zi;
-            v[1] += ri * ri;
+#pragma unroll
+        for (int u = 0; u < kRPL; ++u) {
+            const uint64_t k = b * kBJ + u * 32 + lane;
+            if (k < m) {
+                z[i[u]] = zi[u];
+                if (INIT) p[i[u]] = zi[u];
+                v[0] += ri[u] * zi[u];
+                v[1] += ri[u] * ri[u];
+            }
         }
     }
     double out[2];
@@ -528,6 +549,8 @@ __global__ void permute_kernel(const uint32_t* __restrict__ perm, uint64_t m, co
     }
 }
 
+constexpr int kBJSetupSmem = 2 * kBJ * (kBJ + 1) * (int)sizeof(double);
+
 // Grid of a grid-stride kernel: at most one full wave of resident CTAs (a
 // partial second wave leaves SMs idle at the tail of every launch).
 template <typename K>
@@ -564,6 +587,7 @@ void bj_build_order(rbg_ctx* ctx) {
     bj_pos_kernel<<<blocks_for(m, 256), 256, 0, st>>>(ctx->bj_perm.p, m, ctx->bj_pos.p);
     RBG_CHECK_LAUNCH(ctx);
     RBG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end
+    RBG_CUDA(cudaFuncSetAttribute(bj_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBJSetupSmem));
     ctx->bj_nblk = (m + kBJ - 1) / kBJ;
     ctx->bj_inv.reserve(ctx->bj_nblk * kBJ * kBJ);
     {
@@ -698,7 +722,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
                                                     ctx->ticket.p, ctx->scal.p, tol * tol);
             RBG_CHECK_LAUNCH(ctx);
             if (use_bj) {
-                bj_setup_kernel<<<(unsigned)ctx->bj_nblk, kBJ, 0, st>>>(ctx->uptr.p, ctx->ucols.p, uvals, m,
+                bj_setup_kernel<<<(unsigned)ctx->bj_nblk, kBJ, kBJSetupSmem, st>>>(ctx->uptr.p, ctx->ucols.p, uvals, m,
                                                                         ctx->bj_perm.p, ctx->bj_pos.p, ctx->scal.p,
                                                                         ctx->bj_inv.p);
                 RBG_CHECK_LAUNCH(ctx);
