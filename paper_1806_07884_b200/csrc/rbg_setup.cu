@@ -367,6 +367,7 @@ void setup_centres(rbg_ctx* ctx) {
     ctx->nnz_full = hfptr[m];
     uint32_t max_row = 0;
     for (uint64_t i = 0; i < m; ++i) max_row = std::max<uint32_t>(max_row, (uint32_t)(hfptr[i + 1] - hfptr[i]));
+    ctx->max_full_row = max_row;
     if (max_row >= 0xffff)
         throw Error(RBG_INVALID_ARGUMENT, "pattern row of " + std::to_string(max_row) +
                                               " centres exceeds the 65534-entry slot-map limit");

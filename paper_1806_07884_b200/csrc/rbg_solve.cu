@@ -511,6 +511,8 @@ __global__ void __launch_bounds__(kThreads) bj_update_kernel(uint64_t m, uint64_
     }
 }
 
+constexpr int kKeyShift = 12;  // row offsets < 4096 (the segmented-sort limit)
+
 // Full CSR in Morton order: new row k = centre perm[k], columns renumbered by
 // pos (unsorted within the row: the SpMV does not need it), f2u carried along.
 __global__ void perm_len_kernel(const uint64_t* __restrict__ fptr, const uint64_t* __restrict__ uptr,
@@ -523,6 +525,11 @@ __global__ void perm_len_kernel(const uint64_t* __restrict__ fptr, const uint64_
     }
 }
 
+// SORTED: pass 1 writes keys (new column << 12 | source offset in the row) for a
+// segmented sort, pass 2 (perm_unpack_kernel) turns the sorted keys into
+// columns ascending in Morton position -- a warp's gathers of p then fall on
+// few L2 sectors.
+template <bool SORTED>
 __global__ void perm_fill_kernel(const uint64_t* __restrict__ fptr, const uint32_t* __restrict__ fcols,
                                  const uint64_t* __restrict__ f2u, const uint32_t* __restrict__ perm,
                                  const uint32_t* __restrict__ pos, uint64_t m, const uint64_t* __restrict__ pfptr,
@@ -533,8 +540,27 @@ __global__ void perm_fill_kernel(const uint64_t* __restrict__ fptr, const uint32
         const uint32_t i = perm[k];
         const uint64_t s0 = fptr[i], n = fptr[i + 1] - s0, d0 = pfptr[k];
         for (uint64_t e = lane; e < n; e += 32) {
-            pfcols[d0 + e] = pos[fcols[s0 + e]];
-            pf2u[d0 + e] = f2u[s0 + e];
+            if (SORTED) {
+                pfcols[d0 + e] = (pos[fcols[s0 + e]] << kKeyShift) | (uint32_t)e;
+            } else {
+                pfcols[d0 + e] = pos[fcols[s0 + e]];
+                pf2u[d0 + e] = f2u[s0 + e];
+            }
+        }
+    }
+}
+
+__global__ void perm_unpack_kernel(const uint64_t* __restrict__ fptr, const uint64_t* __restrict__ f2u,
+                                   const uint32_t* __restrict__ perm, uint64_t m, const uint64_t* __restrict__ pfptr,
+                                   uint32_t* __restrict__ pfcols, uint64_t* __restrict__ pf2u) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t k = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5); k < m; k += warps) {
+        const uint64_t s0 = fptr[perm[k]], d0 = pfptr[k], n = pfptr[k + 1] - d0;
+        for (uint64_t e = lane; e < n; e += 32) {
+            const uint32_t key = pfcols[d0 + e];
+            pfcols[d0 + e] = key >> kKeyShift;
+            pf2u[d0 + e] = f2u[s0 + (key & ((1u << kKeyShift) - 1u))];
         }
     }
 }
@@ -601,9 +627,20 @@ void bj_build_order(rbg_ctx* ctx) {
                                                            ctx->puptr.p);
         RBG_CHECK_LAUNCH(ctx);
         exclusive_scan_u32_to_u64(ctx, len.p, ctx->pfptr.p, m);
-        perm_fill_kernel<<<blocks_for(m, 8, 148u * 16u), 256, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->f2u.p,
-                                                                      ctx->bj_perm.p, ctx->bj_pos.p, m, ctx->pfptr.p,
-                                                                      ctx->pfcols.p, ctx->pf2u.p);
+        const unsigned gf = blocks_for(m, 8, 148u * 16u);
+        const bool sorted = m <= (1ull << (32 - kKeyShift)) && ctx->max_full_row <= (1u << kKeyShift) &&
+                            !std::getenv("RBG_PERM_UNSORTED");
+        if (sorted) {
+            perm_fill_kernel<true><<<gf, 256, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->f2u.p, ctx->bj_perm.p,
+                                                       ctx->bj_pos.p, m, ctx->pfptr.p, ctx->pfcols.p, ctx->pf2u.p);
+            RBG_CHECK_LAUNCH(ctx);
+            segmented_sort_u32(ctx, ctx->pfcols.p, ctx->pfptr.p, m, ctx->max_full_row);
+            perm_unpack_kernel<<<gf, 256, 0, st>>>(ctx->fptr.p, ctx->f2u.p, ctx->bj_perm.p, m, ctx->pfptr.p,
+                                                   ctx->pfcols.p, ctx->pf2u.p);
+        } else {
+            perm_fill_kernel<false><<<gf, 256, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->f2u.p, ctx->bj_perm.p,
+                                                        ctx->bj_pos.p, m, ctx->pfptr.p, ctx->pfcols.p, ctx->pf2u.p);
+        }
         RBG_CHECK_LAUNCH(ctx);
         RBG_CUDA(cudaStreamSynchronize(st));
     }
