@@ -51,6 +51,11 @@ const char* rbg_last_error(const rbg_ctx* ctx);
  * the context's own stream. */
 rbg_status rbg_set_stream(rbg_ctx* ctx, void* cuda_stream);
 rbg_status rbg_synchronize(rbg_ctx* ctx);
+/* The CUDA stream (cudaStream_t) all work of the context is issued on: an
+ * external all-reduce of rbg_system_device must be enqueued on it (or be
+ * ordered with it) -- e.g. ncclAllReduce(..., stream) -- so that it runs after
+ * the assembly and before rbg_get_system / rbg_solve. */
+rbg_status rbg_get_stream(rbg_ctx* ctx, void** cuda_stream);
 /* Number of kernel launches issued by this context so far (bench evidence). */
 uint64_t rbg_launch_count(const rbg_ctx* ctx);
 
@@ -62,7 +67,8 @@ uint64_t rbg_launch_count(const rbg_ctx* ctx);
  * assemble_submatrix (coo.cpp:168-175).  Builds the uniform tile grid, the
  * per-tile centre lists (evaluation) and the upper CSR pattern {(i,j): i<=j,
  * |c_i-c_j|^2 < (2/alpha)^2}; the assembly layout (super/sub-tiles, slot
- * maps) follows at the first assembly. */
+ * maps) follows at the first assembly.  Calling it again with an identical
+ * centre set, family and alpha keeps all of it (no device work). */
 rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_t m,
                            int kernel_family, double alpha);
 
@@ -179,8 +185,12 @@ rbg_status rbg_support_counts(rbg_ctx* ctx, const double* points, uint64_t nq, u
                               uint64_t* sum_k2);
 /* fp64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flops), microbenchmark. */
 rbg_status rbg_fp64_peak(rbg_ctx* ctx, double* tflops);
-/* Correctly rounded sqrt used by the tiled kernel vs __dsqrt_rn on 2n inputs. */
-rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
+/* The assembly kernel's phi (exact inclusion, value within a few ulp) against
+ * the reference arithmetic (kernel.hpp:42-62 with sqrt_rn, kdtree.cpp:64,74)
+ * on n sampled distances of every magnitude: inclusion mismatches (must be 0),
+ * max relative error where 1 - t >= 1e-3, max absolute error. */
+rbg_status rbg_phi_selftest(rbg_ctx* ctx, int kernel_family, double alpha, uint64_t n, uint64_t seed,
+                            uint64_t* mismatches, double* max_rel, double* max_abs);
 /* Assembly layout knobs (performance only; results are unaffected beyond
  * fp64 summation order): sub-tile edge = support radius / divisor (1..16,
  * 0 = automatic from the point density) and super-tile = S x S (x S)

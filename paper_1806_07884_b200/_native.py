@@ -89,6 +89,7 @@ _SIGS = {
     "rbg_last_error": (C.c_char_p, [_P]),
     "rbg_set_stream": (C.c_int, [_P, _P]),
     "rbg_synchronize": (C.c_int, [_P]),
+    "rbg_get_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "rbg_launch_count": (_U64, [_P]),
     "rbg_set_centres": (C.c_int, [_P, C.c_int, _P, _U64, C.c_int, C.c_double]),
     "rbg_get_pattern_info": (C.c_int, [_P, C.POINTER(PatternInfo)]),
@@ -107,7 +108,8 @@ _SIGS = {
     "rbg_support_counts": (C.c_int, [_P, _P, _U64, C.POINTER(_U64), C.POINTER(_U64)]),
     "rbg_fp64_peak": (C.c_int, [_P, _D]),
     "rbg_assembly_times": (C.c_int, [_P, _D, _D]),
-    "rbg_sqrt_selftest": (C.c_int, [_P, _U64, _U64, C.POINTER(_U64)]),
+    "rbg_phi_selftest": (C.c_int, [_P, C.c_int, C.c_double, _U64, _U64, C.POINTER(_U64),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "rbg_set_tile_divisor": (C.c_int, [_P, C.c_double]),
     "rbg_set_super_factor": (C.c_int, [_P, C.c_int]),
     "rbg_get_layout_info": (C.c_int, [_P, C.POINTER(LayoutInfo)]),

@@ -115,16 +115,25 @@ class Engine:
         self._check(self._L.rbg_get_layout_info(self._ctx, C.byref(info)))
         return {k: getattr(info, k) for k, _ in info._fields_}
 
-    def sqrt_selftest(self, n: int = 1 << 24, seed: int = 1) -> int:
-        bad = C.c_uint64()
-        self._check(self._L.rbg_sqrt_selftest(self._ctx, n, seed, C.byref(bad)))
-        return int(bad.value)
+    def phi_selftest(self, family: int, alpha: float, n: int = 1 << 24, seed: int = 1) -> dict:
+        """The assembly kernel's phi against the reference arithmetic (rbg_phi_selftest)."""
+        bad, rel, ab = C.c_uint64(), C.c_double(), C.c_double()
+        self._check(self._L.rbg_phi_selftest(self._ctx, int(family), float(alpha), n, seed, C.byref(bad),
+                                             C.byref(rel), C.byref(ab)))
+        return {"mismatches": int(bad.value), "max_rel": rel.value, "max_abs": ab.value}
 
     def set_stream(self, stream: int | None) -> None:
         self._check(self._L.rbg_set_stream(self._ctx, stream))
 
     def synchronize(self) -> None:
         self._check(self._L.rbg_synchronize(self._ctx))
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t the engine issues on (rbg_get_stream)."""
+        s = C.c_void_p()
+        self._check(self._L.rbg_get_stream(self._ctx, C.byref(s)))
+        return int(s.value or 0)
 
     @property
     def launch_count(self) -> int:
@@ -370,8 +379,7 @@ def evaluate_model(model: Model, queries, engine: Engine | None = None) -> np.nd
     if any(model.offset):
         q = q - np.asarray(model.offset[: q.shape[1]])
     eng = engine or Engine()
-    if eng.m != model.refs.shape[0] or eng.kernel is None or eng.kernel.alpha != model.kernel.alpha:
-        eng.set_centres(model.refs, model.kernel)
+    eng.set_centres(model.refs, model.kernel)  # no device work when the engine already holds this set
     eng.set_model_poly(model.poly)
     return eng.evaluate(model.weights, q)
 
@@ -386,8 +394,7 @@ def error_report(model: Model, points, values, design_nnz: int | None = None,
     if h.shape[0] != pts.shape[0]:
         raise ValueError("error_report: cloud value count mismatch")
     eng = engine or Engine()
-    if eng.m != model.refs.shape[0] or eng.kernel is None or eng.kernel.alpha != model.kernel.alpha:
-        eng.set_centres(model.refs, model.kernel)
+    eng.set_centres(model.refs, model.kernel)  # no device work when the engine already holds this set
     eng.set_model_poly(model.poly)
     rep = eng.error_report(model.weights, pts, h, signed=True)
     if design_nnz is not None:

@@ -115,12 +115,37 @@ double NormalSystem::at(std::size_t i, std::size_t j) const {
     return (it != e && *it == j) ? values[static_cast<std::size_t>(it - cols.begin())] : 0.0;
 }
 
-NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
-                                 const KernelSpec& kernel, bool poly, BuildStats* stats,
-                                 Device* device, const AllReduce& allreduce) {
-    if (cloud.values.size() != cloud.points.size())  // solver.cpp:135-136
-        throw std::invalid_argument("build_normal_system: value count does not match points");
-    if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
+PointIndex::PointIndex(std::vector<Point2> points) : points_(std::move(points)) {
+    if (points_.empty()) throw std::invalid_argument("point index requires at least one point");  // kdtree.cpp:11-17
+    if (points_.size() > 0xffffffffull) throw std::invalid_argument("point index limited to 2^32-1 points");
+    for (std::size_t i = 0; i < points_.size(); ++i)
+        if (!std::isfinite(points_[i].x) || !std::isfinite(points_[i].y))
+            throw std::invalid_argument("non-finite coordinate at point index " + std::to_string(i));
+}
+
+namespace {
+
+// The caller's hook runs the all-reduce on the context's stream (rbfit_gpu.hpp).
+void run_allreduce(rbg_ctx* ctx, const AllReduce& allreduce) {
+    if (!allreduce) return;
+    double* buf = nullptr;
+    std::uint64_t count = 0;
+    void* stream = nullptr;
+    check(rbg_system_device(ctx, &buf, &count), ctx);
+    check(rbg_get_stream(ctx, &stream), ctx);
+    allreduce(buf, count, stream);
+}
+
+void check_plan(const BlockPlan& plan, std::size_t m) {  // solver.cpp:137-144
+    if (plan.m_total != m)
+        throw std::invalid_argument("build_normal_system: plan was made for a different reference count");
+    if (plan.block_size == 0 || plan.block_size > m || plan.n_blocks == 0)
+        throw std::invalid_argument("build_normal_system: malformed block plan");
+}
+
+NormalSystem build_on_device(std::span<const Point2> pts, std::span<const double> values,
+                             std::span<const Point2> refs, const KernelSpec& kernel, bool poly,
+                             BuildStats* stats, Device* device, const AllReduce& allreduce, bool validate) {
     Using u(device);
     rbg_ctx* ctx = u.ctx();
     BuildStats local{};
@@ -129,13 +154,8 @@ NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2
     check(rbg_set_poly(ctx, poly ? 1 : 0), ctx);
     local.index_seconds = seconds_since(t0);
     t0 = Clock::now();
-    check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
-    if (allreduce) {
-        double* buf = nullptr;
-        std::uint64_t count = 0;
-        check(rbg_system_device(ctx, &buf, &count), ctx);
-        allreduce(buf, count, nullptr);
-    }
+    check(rbg_assemble(ctx, flat(pts), values.data(), pts.size(), 0, validate ? 1 : 0), ctx);
+    run_allreduce(ctx, allreduce);
     rbg_pattern_info info{};
     check(rbg_get_pattern_info(ctx, &info), ctx);
     const std::size_t m = refs.size();
@@ -164,6 +184,39 @@ NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2
     local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);
     if (stats) *stats = local;
     return sys;
+}
+
+}  // namespace
+
+NormalSystem build_normal_system(const PointIndex& index, std::span<const double> values,
+                                 std::span<const Point2> refs, const KernelSpec& kernel,
+                                 const BlockPlan& plan, bool poly, BuildStats* stats, Device* device,
+                                 const AllReduce& allreduce) {
+    if (values.size() != index.size())  // solver.cpp:133-134
+        throw std::invalid_argument("build_normal_system: value count does not match points");
+    if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
+    check_plan(plan, refs.size());
+    // the index already validated its points (kdtree.cpp:14-17)
+    return build_on_device(index.points(), values, refs, kernel, poly, stats, device, allreduce, false);
+}
+
+NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
+                                 const KernelSpec& kernel, const BlockPlan& plan, bool poly,
+                                 BuildStats* stats, Device* device, const AllReduce& allreduce) {
+    if (cloud.values.size() != cloud.points.size())
+        throw std::invalid_argument("build_normal_system: value count does not match points");
+    if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
+    check_plan(plan, refs.size());
+    return build_on_device(cloud.points, cloud.values, refs, kernel, poly, stats, device, allreduce, true);
+}
+
+NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
+                                 const KernelSpec& kernel, bool poly, BuildStats* stats, Device* device,
+                                 const AllReduce& allreduce) {
+    if (cloud.values.size() != cloud.points.size())  // solver.cpp:135-136
+        throw std::invalid_argument("build_normal_system: value count does not match points");
+    if (refs.empty()) throw std::invalid_argument("build_normal_system: no reference points");
+    return build_on_device(cloud.points, cloud.values, refs, kernel, poly, stats, device, allreduce, true);
 }
 
 Weights solve_weights(const NormalSystem& sys, SolveDiag* diag, Device* device) {
@@ -210,20 +263,15 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     const std::size_t m = refs.size();
     local.plan = BlockPlan{m, m, 1, options.ram_budget_bytes, options.prec_bytes, true};
 
-    Device dev(options.device);
-    rbg_ctx* ctx = dev.ctx();
+    Using u(options.engine, options.device);
+    rbg_ctx* ctx = u.ctx();
     auto t0 = Clock::now();
     set_centres(ctx, refs, kernel);
     check(rbg_set_poly(ctx, options.poly ? 1 : 0), ctx);
     local.index_seconds = seconds_since(t0);
     t0 = Clock::now();
     check(rbg_assemble(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), 0, 1), ctx);
-    if (options.allreduce) {
-        double* buf = nullptr;
-        std::uint64_t count = 0;
-        check(rbg_system_device(ctx, &buf, &count), ctx);
-        options.allreduce(buf, count, nullptr);
-    }
+    run_allreduce(ctx, options.allreduce);
     std::vector<double> hits(m);
     std::uint64_t design_nnz = 0;
     check(rbg_get_system(ctx, nullptr, nullptr, hits.data(), &design_nnz), ctx);
@@ -257,6 +305,53 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     Model model{kernel, std::move(refs), std::move(c), poly, cloud.offset};
     if (report) *report = std::move(local);
     return model;
+}
+
+std::vector<BenchRow> bench_block_sizes(const PointCloud& cloud, std::vector<Point2> refs,
+                                        const KernelSpec& kernel, const FitOptions& options,
+                                        std::span<const std::size_t> block_sizes, double* index_seconds) {
+    if (block_sizes.empty()) throw std::invalid_argument("bench_block_sizes: no block sizes given");  // solver.cpp:484-487
+    if (cloud.size() == 0) throw std::invalid_argument("bench_block_sizes: empty cloud");
+    if (refs.empty()) throw std::invalid_argument("bench_block_sizes: no reference points");
+    const auto t0 = Clock::now();
+    const PointIndex index(cloud.points);
+    if (index_seconds) *index_seconds = seconds_since(t0);
+    Using u(options.engine, options.device);
+    const std::size_t m = refs.size();
+    std::vector<BenchRow> rows;
+    NormalSystem baseline;
+    for (const std::size_t requested : block_sizes) {
+        const std::size_t mb = std::clamp<std::size_t>(requested, 1, m);
+        const BlockPlan plan{m, mb, (m + mb - 1) / mb, options.ram_budget_bytes, options.prec_bytes, false};
+        BuildStats stats{};
+        NormalSystem sys = build_normal_system(index, cloud.values, refs, kernel, plan, options.poly, &stats,
+                                               u.dev, options.allreduce);
+        const auto ts = Clock::now();
+        Weights w = solve_weights(sys, nullptr, u.dev);
+        const double solve_seconds = seconds_since(ts);
+        const Model model{kernel, refs, std::move(w.c), w.poly, cloud.offset};
+        const ErrorReport er = error_report(model, cloud, stats.design_nnz, u.dev);
+        BenchRow row;
+        row.block_size = mb;
+        row.n_blocks = plan.n_blocks;
+        row.assembly_seconds = stats.assembly_seconds;
+        row.gram_solve_seconds = stats.gram_seconds + solve_seconds;
+        row.mae = er.mean_absolute_error;
+        if (rows.empty()) {
+            baseline = std::move(sys);
+        } else {
+            double worst = 0.0;
+            const auto update = [&worst](double a, double b) {
+                const double mag = std::max(std::abs(a), std::abs(b));
+                if (mag > 0.0) worst = std::max(worst, std::abs(a - b) / mag);
+            };
+            for (std::size_t i = 0; i < baseline.values.size(); ++i) update(baseline.values[i], sys.values[i]);
+            for (std::size_t i = 0; i < baseline.rhs.size(); ++i) update(baseline.rhs[i], sys.rhs[i]);
+            row.max_rel_diff = worst;
+        }
+        rows.push_back(row);
+    }
+    return rows;
 }
 
 std::vector<double> evaluate_model(const Model& model, std::span<const Point2> queries,

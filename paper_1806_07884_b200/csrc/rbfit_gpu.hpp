@@ -75,6 +75,19 @@ class Device {
     rbg_ctx* ctx_ = nullptr;
 };
 
+// PointIndex (kdtree.hpp:10-28): owns a copy of the points and validates them
+// like the reference (kdtree.cpp:10-17); the spatial index itself is the
+// device-side binning done per assembly, so no tree is built on the host.
+class PointIndex {
+  public:
+    explicit PointIndex(std::vector<Point2> points);
+    std::size_t size() const { return points_.size(); }
+    const std::vector<Point2>& points() const { return points_; }
+
+  private:
+    std::vector<Point2> points_;
+};
+
 // NormalSystem (solver.hpp:61-69) in upper-CSR form.
 struct NormalSystem {
     std::size_t side = 0;
@@ -101,10 +114,31 @@ struct BuildStats {  // solver.hpp:71-78 (device times)
 };
 
 // Sum-allreduce hook for multi-GPU builds: called with the device buffer
-// [values | rhs | hits] (fp64) after the local slab is assembled, on the
-// context's stream (e.g. wraps ncclAllReduce(..., ncclFloat64, ncclSum)).
+// [values | rhs | hits (| border)] (fp64) after the local slab's assembly has
+// been ENQUEUED, and with `stream` = the context's cudaStream_t
+// (rbg_get_stream).  The hook must enqueue its reduction on that stream (e.g.
+// ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, comm, (cudaStream_t)
+// stream)): the assembly before it and every read after it run on the same
+// stream, so no other synchronisation is needed.
 using AllReduce = std::function<void(double* device_buffer, std::uint64_t count, void* stream)>;
 
+struct BlockPlan {  // solver.hpp:26-33; accepted and validated, one block on the GPU
+    std::size_t m_total = 0, block_size = 0, n_blocks = 1, ram_budget_bytes = 0, prec_bytes = 8;
+    bool sparse_mode = true;
+};
+
+// build_normal_system (solver.hpp:86-94).  The plan is validated with the
+// reference's messages (solver.cpp:135-144) and otherwise has no effect: the
+// whole pattern is resident on the device.
+NormalSystem build_normal_system(const PointIndex& index, std::span<const double> values,
+                                 std::span<const Point2> refs, const KernelSpec& kernel,
+                                 const BlockPlan& plan, bool poly, BuildStats* stats = nullptr,
+                                 Device* device = nullptr, const AllReduce& allreduce = {});
+NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
+                                 const KernelSpec& kernel, const BlockPlan& plan, bool poly,
+                                 BuildStats* stats = nullptr, Device* device = nullptr,
+                                 const AllReduce& allreduce = {});
+// Convenience form without a plan (one block).
 NormalSystem build_normal_system(const PointCloud& cloud, std::span<const Point2> refs,
                                  const KernelSpec& kernel, bool poly, BuildStats* stats = nullptr,
                                  Device* device = nullptr, const AllReduce& allreduce = {});
@@ -132,12 +166,8 @@ struct FitOptions {  // solver.hpp:113-118 (+ GPU solve controls)
     double tol = 1e-12;
     int max_iter = 20000;
     int device = 0;
-    AllReduce allreduce;  // multi-GPU: sum partial systems across ranks
-};
-
-struct BlockPlan {
-    std::size_t m_total = 0, block_size = 0, n_blocks = 1, ram_budget_bytes = 0, prec_bytes = 8;
-    bool sparse_mode = true;
+    Device* engine = nullptr;  // the caller's context (and its stream); `device` is then ignored
+    AllReduce allreduce;       // multi-GPU: sum partial systems across ranks (see AllReduce)
 };
 
 struct FitReport {  // solver.hpp:120-131
@@ -164,6 +194,24 @@ struct Model {  // model.hpp:17-23
 
 Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& kernel,
           const FitOptions& options = {}, FitReport* report = nullptr);
+
+struct BenchRow {  // solver.hpp:133-142
+    std::size_t block_size = 0;
+    std::size_t n_blocks = 0;
+    double assembly_seconds = 0.0;
+    double gram_solve_seconds = 0.0;
+    double mae = 0.0;
+    double max_rel_diff = 0.0;  // (b, rhs) against the first run
+};
+
+// bench_block_sizes (solver.hpp:144-150, solver.cpp:480-536): one GPU fit per
+// requested block size.  The GPU assembles every plan as one block, so the
+// rows time repeated fits and max_rel_diff checks run-to-run agreement of the
+// assembled system (summation order only).
+std::vector<BenchRow> bench_block_sizes(const PointCloud& cloud, std::vector<Point2> refs,
+                                        const KernelSpec& kernel, const FitOptions& options,
+                                        std::span<const std::size_t> block_sizes,
+                                        double* index_seconds = nullptr);
 
 std::vector<double> evaluate_model(const Model& model, std::span<const Point2> queries,
                                    Device* device = nullptr);

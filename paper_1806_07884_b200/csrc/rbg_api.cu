@@ -39,6 +39,20 @@ void require_centres(const rbg_ctx* ctx) {
     if (!ctx->have_centres)
         throw Error(RBG_NOT_READY, "no reference points set (call rbg_set_centres first)");
 }
+// The symbolic pattern (K2) is built at the first call that needs it.
+void require_pattern(rbg_ctx* ctx) {
+    require_centres(ctx);
+    if (ctx->have_pattern) return;
+    RBG_CUDA(cudaSetDevice(ctx->device));
+    RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    rbg::setup_pattern(ctx);
+    RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    RBG_CUDA(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->setup_ms += ms;
+}
+
 void require_system(const rbg_ctx* ctx) {
     require_centres(ctx);
     if (!ctx->have_system)
@@ -57,8 +71,7 @@ void check_misses(rbg_ctx* ctx) {
     unsigned long long miss = 0;
     RBG_CUDA(cudaMemcpyAsync(&miss, ctx->counters.p, sizeof(miss), cudaMemcpyDeviceToHost, ctx->stream));
     RBG_CUDA(cudaStreamSynchronize(ctx->stream));
-    static const bool timing_experiment = std::getenv("RBG_DEBUG_SKIP") != nullptr;  // results invalid by design
-    if (miss && !timing_experiment)
+    if (miss)
         throw Error(RBG_RUNTIME_ERROR, "internal: " + std::to_string(miss) +
                                            " assembly updates fell outside the symbolic pattern");
 }
@@ -142,6 +155,13 @@ rbg_status rbg_set_stream(rbg_ctx* ctx, void* stream) {
     return guarded(ctx, [&] { ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream; });
 }
 
+rbg_status rbg_get_stream(rbg_ctx* ctx, void** stream) {
+    return guarded(ctx, [&] {
+        if (!stream) throw Error(RBG_INVALID_ARGUMENT, "null stream pointer");
+        *stream = (void*)ctx->stream;
+    });
+}
+
 rbg_status rbg_synchronize(rbg_ctx* ctx) {
     return guarded(ctx, [&] {
         bind(ctx);
@@ -164,6 +184,13 @@ rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_
             throw Error(RBG_INVALID_ARGUMENT, "reference count exceeds 32-bit triplet index range");
         check_points_finite(centres, m, dim, "non-finite reference point at index ");  // coo.cpp:172-175
         bind(ctx);
+        // the same centre set and kernel again (e.g. evaluate_model after fit): everything
+        // derived from the centres -- grid, pattern, assembly layout, solver order -- stays
+        if (ctx->have_centres && ctx->dim == dim && ctx->m == m && ctx->family == family &&
+            ctx->alpha == alpha && ctx->host_centres.size() == m * (uint64_t)dim &&
+            std::memcmp(ctx->host_centres.data(), centres, m * dim * sizeof(double)) == 0)
+            return;
+        ctx->host_centres.assign(centres, centres + m * (uint64_t)dim);
         ctx->have_centres = false;
         ctx->have_system = false;
         ctx->dim = dim;
@@ -188,7 +215,7 @@ rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_
 
 rbg_status rbg_get_pattern_info(rbg_ctx* ctx, rbg_pattern_info* info) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         if (!info) throw Error(RBG_INVALID_ARGUMENT, "null info");
         info->m = ctx->m;
         info->nnz_upper = ctx->nnz_upper;
@@ -203,7 +230,7 @@ rbg_status rbg_get_pattern_info(rbg_ctx* ctx, rbg_pattern_info* info) {
 
 rbg_status rbg_get_pattern(rbg_ctx* ctx, uint64_t* row_ptr, uint32_t* cols) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         bind(ctx);
         if (row_ptr)
             RBG_CUDA(cudaMemcpyAsync(row_ptr, ctx->uptr.p, (ctx->m + 1) * sizeof(uint64_t),
@@ -218,7 +245,7 @@ rbg_status rbg_get_pattern(rbg_ctx* ctx, uint64_t* row_ptr, uint32_t* cols) {
 rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uint64_t n,
                         int accumulate, int validate) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
         bind(ctx);
         const int dim = ctx->dim;
@@ -288,7 +315,7 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
 rbg_status rbg_assemble_device(rbg_ctx* ctx, const double* d_points, const double* d_h, uint64_t n,
                                int accumulate) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         bind(ctx);
         rbg::assemble_points(ctx, d_points, d_h, n, accumulate != 0);
     });
@@ -296,7 +323,7 @@ rbg_status rbg_assemble_device(rbg_ctx* ctx, const double* d_points, const doubl
 
 rbg_status rbg_system_device(rbg_ctx* ctx, double** d_buffer, uint64_t* count) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         if (d_buffer) *d_buffer = ctx->sys.p;
         if (count) *count = ctx->sys_count();
     });
@@ -334,7 +361,7 @@ rbg_status rbg_get_system(rbg_ctx* ctx, double* values, double* rhs, double* hit
 
 rbg_status rbg_set_system(rbg_ctx* ctx, const double* values, const double* rhs, const double* hits) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         if (!values || !rhs) throw Error(RBG_INVALID_ARGUMENT, "null system array");
         bind(ctx);
         cudaStream_t st = ctx->stream;
@@ -401,6 +428,8 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
         ctx->ev_h.reserve(n);
         RBG_CUDA(cudaMemcpyAsync(ctx->ev_c.p, c, ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
         rbg::h2d(ctx, ctx->ev_q.p, points, n * ctx->dim * sizeof(double));
+        if (const uint64_t bad = rbg::first_nonfinite(ctx, ctx->ev_q.p, n, ctx->dim); bad < n)  // model.cpp:60
+            throw Error(RBG_INVALID_ARGUMENT, "evaluate_model: non-finite query point at index " + std::to_string(bad));
         rbg::h2d(ctx, ctx->ev_h.p, h, n * sizeof(double));
         rbg::evaluate_points(ctx, ctx->ev_c.p, ctx->ev_q.p, n, ctx->ev_f.p);
         rbg::error_stats(ctx, ctx->ev_f.p, ctx->ev_h.p, n, out);
@@ -413,7 +442,7 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
 
 rbg_status rbg_set_poly(rbg_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         bind(ctx);
         ctx->poly_on = enable != 0;
         ctx->have_system = false;  // the system layout changes
@@ -443,7 +472,7 @@ rbg_status rbg_get_border(rbg_ctx* ctx, double* atp, double* ptp, double* pth) {
 
 rbg_status rbg_set_border(rbg_ctx* ctx, const double* atp, const double* ptp, const double* pth) {
     return guarded(ctx, [&] {
-        require_centres(ctx);
+        require_pattern(ctx);
         const int T = ctx->pterms();
         if (T == 0) throw Error(RBG_INVALID_ARGUMENT, "no polynomial border (call rbg_set_poly first)");
         if (!atp || !ptp || !pth) throw Error(RBG_INVALID_ARGUMENT, "null border array");

@@ -4,6 +4,7 @@
 //  * an fp64 FMA throughput microbenchmark (the fp64 roofline denominator,
 //    which MEASURED_PEAKS.json does not carry).
 #include <algorithm>
+#include <cstring>
 
 #include "rbg_internal.cuh"
 
@@ -44,24 +45,44 @@ __global__ void support_count_kernel(GridDev g, const uint64_t* __restrict__ cpt
     }
 }
 
-// sqrt_rn_nonneg vs __dsqrt_rn on n pseudo-random doubles spread over
-// [2^-60, 2^4) (exponent and mantissa uniform) plus exact squares.
-__global__ void sqrt_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long* bad) {
+// K3's phi (phi_k3) against the reference's exact arithmetic (phi_of_r of
+// the correctly rounded sqrt, strict d2 < r2) on n pseudo-random d2 per
+// class: uniform in [0, 1.02 r2) (mantissa noise), within a few thousand ulp
+// of the inclusion threshold, spread over every exponent down to the
+// subnormals, and exact zero.  out[0] = inclusion mismatches, out[1] = max
+// relative error of phi where (1 - t) >= 1e-3, out[2] = max absolute error.
+template <int FAM>
+__global__ void phi_selftest_kernel(double alpha, double r2, long long ib, uint64_t n, uint64_t seed,
+                                    unsigned long long* mism, double* rel, double* ab) {
     unsigned long long nbad = 0;
+    double mrel = 0.0, mabs = 0.0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t k = (i + 1) * 0x9e3779b97f4a7c15ull ^ seed;
         k ^= k >> 31;
         k *= 0xbf58476d1ce4e5b9ull;
         k ^= k >> 29;
-        const uint64_t mant = k & 0xfffffffffffffull;
-        const uint64_t ex = 1023 - 60 + ((k >> 52) % 64);
-        const double x = __longlong_as_double((long long)((ex << 52) | mant));
-        if (sqrt_rn_nonneg(x) != __dsqrt_rn(x)) ++nbad;
-        const double sq = (double)(i & 0xffffff) * (double)(i & 0xffffff);
-        if (sqrt_rn_nonneg(sq) != __dsqrt_rn(sq)) ++nbad;
+        double d2;
+        switch (i & 3) {
+            case 0: d2 = 1.02 * r2 * ((double)(k >> 11) * 0x1.0p-53); break;
+            case 1: d2 = __longlong_as_double(ib + (long long)(k % 4096) - 2048); break;
+            case 2: d2 = __longlong_as_double((long long)(k % 0x7fe0000000000000ull)); break;  // any exponent
+            default: d2 = (i & 4) ? 0.0 : __longlong_as_double((long long)(k & 0xfffffffffffffull));  // subnormal
+        }
+        if (!(d2 >= 0.0)) continue;
+        bool in;
+        const double v = phi_k3<FAM>(d2, alpha, ib, in);
+        const double r = __dsqrt_rn(d2);
+        const double ex = d2 < r2 ? phi_of_r(FAM, alpha, r) : 0.0;
+        if (in != (ex != 0.0)) ++nbad;
+        const double err = fabs(v - ex);
+        mabs = fmax(mabs, err);
+        if (ex != 0.0 && __dsub_rn(1.0, __dmul_rn(alpha, r)) >= 1e-3) mrel = fmax(mrel, err / ex);
     }
-    if (nbad) atomicAdd(bad, nbad);
+    if (nbad) atomicAdd(mism, nbad);
+    // fp64 >= 0 compares like its bit pattern
+    atomicMax(reinterpret_cast<unsigned long long*>(rel), (unsigned long long)__double_as_longlong(mrel));
+    atomicMax(reinterpret_cast<unsigned long long*>(ab), (unsigned long long)__double_as_longlong(mabs));
 }
 
 constexpr int kChains = 8;
@@ -164,18 +185,32 @@ extern "C" rbg_status rbg_assembly_times(rbg_ctx* ctx, double* bin_ms, double* t
     }
 }
 
-extern "C" rbg_status rbg_sqrt_selftest(rbg_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches) {
-    if (!ctx || !mismatches) return RBG_INVALID_ARGUMENT;
+extern "C" rbg_status rbg_phi_selftest(rbg_ctx* ctx, int family, double alpha, uint64_t n, uint64_t seed,
+                                       uint64_t* mismatches, double* max_rel, double* max_abs) {
+    if (!ctx || !mismatches || family < 0 || family > 3 || !(alpha > 0.0)) return RBG_INVALID_ARGUMENT;
     try {
         RBG_CUDA(cudaSetDevice(ctx->device));
-        ctx->counters.reserve(4);
-        RBG_CUDA(cudaMemsetAsync(ctx->counters.p + 3, 0, sizeof(unsigned long long), ctx->stream));
-        rbg::sqrt_selftest_kernel<<<148 * 16, 256, 0, ctx->stream>>>(n, seed, ctx->counters.p + 3);
+        ctx->counters.reserve(8);
+        cudaStream_t st = ctx->stream;
+        RBG_CUDA(cudaMemsetAsync(ctx->counters.p + 3, 0, 3 * sizeof(unsigned long long), st));
+        const double r2 = (1.0 / alpha) * (1.0 / alpha);
+        const long long ib = rbg::inclusion_bits(alpha, r2);
+        unsigned long long* c = ctx->counters.p + 3;
+        double* rel = reinterpret_cast<double*>(c + 1);
+        double* ab = reinterpret_cast<double*>(c + 2);
+        switch (family) {
+            case 0: rbg::phi_selftest_kernel<0><<<148 * 8, 256, 0, st>>>(alpha, r2, ib, n, seed, c, rel, ab); break;
+            case 1: rbg::phi_selftest_kernel<1><<<148 * 8, 256, 0, st>>>(alpha, r2, ib, n, seed, c, rel, ab); break;
+            case 2: rbg::phi_selftest_kernel<2><<<148 * 8, 256, 0, st>>>(alpha, r2, ib, n, seed, c, rel, ab); break;
+            default: rbg::phi_selftest_kernel<3><<<148 * 8, 256, 0, st>>>(alpha, r2, ib, n, seed, c, rel, ab);
+        }
         RBG_CHECK_LAUNCH(ctx);
-        unsigned long long h = 0;
-        RBG_CUDA(cudaMemcpyAsync(&h, ctx->counters.p + 3, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-        RBG_CUDA(cudaStreamSynchronize(ctx->stream));
-        *mismatches = h;
+        unsigned long long h[3];
+        RBG_CUDA(cudaMemcpyAsync(h, c, sizeof(h), cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        *mismatches = h[0];
+        if (max_rel) std::memcpy(max_rel, &h[1], sizeof(double));
+        if (max_abs) std::memcpy(max_abs, &h[2], sizeof(double));
         return RBG_OK;
     } catch (const rbg::Error& e) {
         ctx->err = e.what();

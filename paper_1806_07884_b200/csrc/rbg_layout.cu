@@ -263,7 +263,7 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     for (uint64_t T = 0; T < n_super; ++T) {
         const uint64_t l = hcptr[T + 1] - hcptr[T];
         max_ls = std::max<uint32_t>(max_ls, (uint32_t)l);
-        mptr[T + 1] = mptr[T] + ((l * (l + 1) / 2 + 7) & ~7ull);  // 16-B aligned for TMA
+        mptr[T + 1] = mptr[T] + ((l * (l + 1) / 2 + 7) & ~7ull);  // 16-B aligned for the cp.async staging
     }
     L.max_ls = max_ls;
     L.mean_ls = n_super ? (double)total_ids / (double)n_super : 0.0;

@@ -15,6 +15,7 @@
 //     numeric kernel flushes without searching (used by rbg_layout.cu).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <numeric>
 
 #include "rbg_internal.cuh"
@@ -175,6 +176,63 @@ __global__ void full_to_upper_kernel(const uint64_t* __restrict__ fptr,
     }
 }
 
+// Bounding box of the centres: per-warp min/max, then one atomic per warp on
+// an order-preserving integer image of each double.
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+inline double ord_val(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    std::memcpy(&v, &b, sizeof v);
+    return v;
+}
+
+template <int DIM>
+__global__ void bbox_kernel(const double* __restrict__ c, uint64_t m, unsigned long long* __restrict__ out) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        for (int d = 0; d < DIM; ++d) {
+            const double v = c[i * DIM + d];
+            lo[d] = fmin(lo[d], v);
+            hi[d] = fmax(hi[d], v);
+        }
+    for (int d = 0; d < DIM; ++d)
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    if ((threadIdx.x & 31) == 0)
+        for (int d = 0; d < DIM; ++d) {
+            atomicMin(&out[d], ord_key(lo[d]));
+            atomicMax(&out[3 + d], ord_key(hi[d]));
+        }
+}
+
+// Centres -> cells of edge >= 2r (the K2 neighbour grid): counting sort on
+// the cell key (count, scan, scatter); the order inside a cell is irrelevant
+// because every pattern row is sorted afterwards.
+template <int DIM, bool FILL>
+__global__ void cell_bin_kernel(const double* __restrict__ c, uint64_t m, CellDev g,
+                                uint32_t* __restrict__ count, const uint64_t* __restrict__ ptr,
+                                uint32_t* __restrict__ ids) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double lo[3] = {g.lo0, g.lo1, g.lo2};
+        const int64_t n[3] = {g.n0, g.n1, g.n2};
+        uint64_t k = 0;
+        for (int d = DIM - 1; d >= 0; --d) {
+            int64_t cc = (int64_t)floor((c[i * DIM + d] - lo[d]) * g.inv_edge);
+            cc = cc < 0 ? 0 : (cc >= n[d] ? n[d] - 1 : cc);
+            k = k * (uint64_t)n[d] + (uint64_t)cc;
+        }
+        const uint32_t pos = atomicAdd(&count[k], 1u);
+        if (FILL) ids[ptr[k] + pos] = (uint32_t)i;
+    }
+}
+
 // Per (tile, local row a): merge the tile's ascending list with upper row
 // c_a's ascending columns -> packed slot offsets.
 __global__ void tile_map_kernel(const uint64_t* __restrict__ cptr, uint64_t n_tiles,
@@ -254,18 +312,29 @@ void setup_centres(rbg_ctx* ctx) {
     cudaStream_t st = ctx->stream;
     ctx->bj_built = false;  // preconditioner blocks follow the centre set
 
-    // ---- host: bounding box + tile grid plan ------------------------------
-    std::vector<double> hc(m * dim);
-    RBG_CUDA(cudaMemcpyAsync(hc.data(), ctx->centres.p, m * dim * sizeof(double),
-                             cudaMemcpyDeviceToHost, st));
-    RBG_CUDA(cudaStreamSynchronize(st));
+    // ---- bounding box (device reduction) + tile grid plan -------------------
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int d = 0; d < dim; ++d) lo[d] = hi[d] = hc[d];
-    for (uint64_t i = 0; i < m; ++i)
-        for (int d = 0; d < dim; ++d) {
-            lo[d] = std::min(lo[d], hc[i * dim + d]);
-            hi[d] = std::max(hi[d], hc[i * dim + d]);
+    {
+        DevBuf<unsigned long long> bb;
+        bb.reserve(6);
+        unsigned long long init[6];
+        for (int d = 0; d < 3; ++d) {
+            init[d] = ~0ull;
+            init[3 + d] = 0ull;
         }
+        RBG_CUDA(cudaMemcpyAsync(bb.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        const unsigned bbk = blocks_for(m, 256, 148u * 4u);
+        if (dim == 2) bbox_kernel<2><<<bbk, 256, 0, st>>>(ctx->centres.p, m, bb.p);
+        else bbox_kernel<3><<<bbk, 256, 0, st>>>(ctx->centres.p, m, bb.p);
+        RBG_CHECK_LAUNCH(ctx);
+        unsigned long long hb[6];
+        RBG_CUDA(cudaMemcpyAsync(hb, bb.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaStreamSynchronize(st));
+        for (int d = 0; d < dim; ++d) {
+            lo[d] = ord_val(hb[d]);
+            hi[d] = ord_val(hb[3 + d]);
+        }
+    }
     const double r = ctx->radius;
     TileGrid g;
     g.dim = dim;
@@ -304,9 +373,23 @@ void setup_centres(rbg_ctx* ctx) {
     uint32_t max_l = 0;
     for (uint64_t t = 0; t < nt; ++t) max_l = std::max<uint32_t>(max_l, (uint32_t)(cptr[t + 1] - cptr[t]));
     ctx->max_tile_centres = max_l;
-    const unsigned cb = blocks_for(m, 128);
+    for (int d = 0; d < 3; ++d) {
+        ctx->bbox_lo[d] = lo[d];
+        ctx->bbox_hi[d] = hi[d];
+    }
+    ctx->have_pattern = false;  // built at the first call that needs it (setup_pattern)
+    ctx->lay = AsmLayout();     // rebuilt at the next assembly for this centre set
+}
 
-    // ---- K2: pattern --------------------------------------------------------
+// K2: the symbolic pattern of the centre set (upper + full CSR, full->upper map).
+void setup_pattern(rbg_ctx* ctx) {
+    const int dim = ctx->dim;
+    const uint64_t m = ctx->m;
+    cudaStream_t st = ctx->stream;
+    const double r = ctx->radius;
+    const double* lo = ctx->bbox_lo;
+    const double* hi = ctx->bbox_hi;
+    const unsigned cb = blocks_for(m, 128);
     const double two_r = 2.0 * r;
     const double lim = two_r * two_r;
     double cedge = two_r * (1.0 + 1e-9);
@@ -322,35 +405,22 @@ void setup_centres(rbg_ctx* ctx) {
         cedge *= 1.5;
     }
     const double cinv = 1.0 / cedge;
-    std::vector<uint64_t> cell_ptr(ncell + 1, 0);
-    std::vector<uint64_t> key(m);
-    for (uint64_t i = 0; i < m; ++i) {
-        uint64_t k = 0;
-        for (int d = dim - 1; d >= 0; --d) {
-            int64_t cc = (int64_t)std::floor((hc[i * dim + d] - lo[d]) * cinv);
-            cc = std::max<int64_t>(0, std::min<int64_t>(cn[d] - 1, cc));
-            k = k * (uint64_t)cn[d] + (uint64_t)cc;
-        }
-        key[i] = k;
-        ++cell_ptr[k + 1];
-    }
-    for (uint64_t cidx = 0; cidx < ncell; ++cidx) cell_ptr[cidx + 1] += cell_ptr[cidx];
-    std::vector<uint32_t> cell_ids(m);
-    {
-        std::vector<uint64_t> cur(cell_ptr.begin(), cell_ptr.end() - 1);
-        for (uint64_t i = 0; i < m; ++i) cell_ids[cur[key[i]]++] = (uint32_t)i;
-    }
+    CellDev cd{lo[0], lo[1], lo[2], cinv, cn[0], cn[1], cn[2]};
     DevBuf<uint64_t> d_cell_ptr;
     DevBuf<uint32_t> d_cell_ids, d_len, d_diag;
     d_cell_ptr.reserve(ncell + 1);
     d_cell_ids.reserve(m);
-    d_len.reserve(m + 1);
+    d_len.reserve(std::max<uint64_t>(m, ncell) + 1);
     d_diag.reserve(m);
-    RBG_CUDA(cudaMemcpyAsync(d_cell_ptr.p, cell_ptr.data(), (ncell + 1) * sizeof(uint64_t),
-                             cudaMemcpyHostToDevice, st));
-    RBG_CUDA(cudaMemcpyAsync(d_cell_ids.p, cell_ids.data(), m * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, st));
-    CellDev cd{lo[0], lo[1], lo[2], cinv, cn[0], cn[1], cn[2]};
+    RBG_CUDA(cudaMemsetAsync(d_len.p, 0, (ncell + 1) * sizeof(uint32_t), st));
+    if (dim == 2) cell_bin_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_len.p, nullptr, nullptr);
+    else cell_bin_kernel<3, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_len.p, nullptr, nullptr);
+    RBG_CHECK_LAUNCH(ctx);
+    exclusive_scan_u32_to_u64(ctx, d_len.p, d_cell_ptr.p, ncell);
+    RBG_CUDA(cudaMemsetAsync(d_len.p, 0, (ncell + 1) * sizeof(uint32_t), st));
+    if (dim == 2) cell_bin_kernel<2, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_len.p, d_cell_ptr.p, d_cell_ids.p);
+    else cell_bin_kernel<3, true><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_len.p, d_cell_ptr.p, d_cell_ids.p);
+    RBG_CHECK_LAUNCH(ctx);
     ctx->fptr.reserve(m + 1);
     if (dim == 2)
         pattern_rows_kernel<2, false><<<cb, 128, 0, st>>>(ctx->centres.p, m, cd, d_cell_ptr.p,
@@ -398,13 +468,12 @@ void setup_centres(rbg_ctx* ctx) {
                                              ctx->ucols.p, ctx->f2u.p);
     RBG_CHECK_LAUNCH(ctx);
 
-    ctx->lay = AsmLayout();  // rebuilt at the next assembly for this centre set
-
     // ---- system + point workspace sized for this centre set ----------------
     ctx->sys.reserve(ctx->nnz_upper + 2 * m + 4 * m + 20);  // room for the polynomial border
     ctx->counters.reserve(4);
     RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
     RBG_CUDA(cudaStreamSynchronize(st));
+    ctx->have_pattern = true;
 }
 
 }  // namespace rbg

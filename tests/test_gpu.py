@@ -212,9 +212,17 @@ def test_cfg2_full_size_properties(eng):
     del B
 
 
-def test_branchfree_sqrt_is_correctly_rounded(eng):
-    # the tiled kernel's sqrt must be bitwise __dsqrt_rn (A entries bitwise)
-    assert eng.sqrt_selftest(1 << 26, 12345) == 0
+@pytest.mark.parametrize("family", [0, 1, 2, 3])
+def test_assembly_phi_inclusion_exact_and_value_close(eng, family):
+    """phi_k3 (the assembly kernel's phi): inclusion bit-exact against the
+    reference rule (kdtree.cpp:64,74 + kernel.hpp:45-46) over distances of
+    every magnitude incl. 0, subnormals and the threshold's neighbourhood;
+    value within 1e-14 relative where 1 - t >= 1e-3."""
+    for alpha in (0.25, 1.0, 10.2333, 280.2496, 1e6):
+        r = eng.phi_selftest(family, alpha, 1 << 24, 12345)
+        assert r["mismatches"] == 0, (alpha, r)
+        assert r["max_rel"] < 1e-14, (alpha, r)
+        assert r["max_abs"] < 1e-13 * (3.0 if family == 3 else 1.0), (alpha, r)
 
 
 @pytest.mark.parametrize("div,sup", [(2.0, 1), (3.0, 2), (5.0, 3), (6.0, 4), (8.0, 2), (12.0, 5)])

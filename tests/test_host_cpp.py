@@ -77,3 +77,28 @@ def test_host_layer_poly_affine_reproduction(exe, tmp_path):
     assert d[0] < 1e-8
     assert np.allclose(d[1:4], [2.0, 3.0, 1.0], atol=1e-6)
     assert np.allclose(d[-3:], d[1:4], rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_allreduce_hook_runs_on_the_context_stream(tmp_path):
+    """rbfit_b200::AllReduce gets the context's stream (rbg_get_stream): a hook
+    that only enqueues an add of a second context's partial system on that
+    stream reproduces the single-pass assembly (rbfit_gpu.hpp; the NCCL
+    all-reduce of SURVEY 8(e) plugs in the same way)."""
+    from paper_1806_07884_b200 import configs
+    exe = tmp_path / "hook_check"
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-std=c++20", "-O2", "-gencode", "arch=compute_100a,code=sm_100a",
+                    f"-I{PKG / 'csrc'}", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / "hook_check.cu"),
+                    "-o", str(exe), f"-L{PKG}", "-lrbfit_b200", "-lrbg", f"-Xlinker=-rpath,{PKG}"], check=True)
+    cfg = configs.CONFIGS["cfg2"]
+    xy, h = configs.points("cfg2", n=400_000)
+    refs = configs.centres("cfg2")
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        np.array([len(h), len(refs)], dtype=np.uint64).tofile(f)
+        np.array([cfg.alpha]).tofile(f)
+        xy.tofile(f)
+        h.tofile(f)
+        refs.tofile(f)
+    r = subprocess.run([str(exe), str(inp)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

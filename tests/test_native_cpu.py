@@ -43,7 +43,8 @@ def test_host_layer_library_exports_reference_api():
     for name in ("rbfit_b200::fit(", "rbfit_b200::build_normal_system(", "rbfit_b200::solve_weights(",
                  "rbfit_b200::evaluate_model(", "rbfit_b200::error_report(", "rbfit_b200::KernelSpec::evaluate",
                  "rbfit_b200::save_model(", "rbfit_b200::load_model(", "rbfit_b200::load_xyz(",
-                 "rbfit_b200::save_xyz(", "rbfit_b200::write_signed_errors(", "rbfit_b200::center_cloud("):
+                 "rbfit_b200::save_xyz(", "rbfit_b200::write_signed_errors(", "rbfit_b200::center_cloud(",
+                 "rbfit_b200::bench_block_sizes(", "rbfit_b200::PointIndex::PointIndex("):
         assert name in out, name
 
 
