@@ -6,6 +6,9 @@
 #include "rbf_oracle.h"
 
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -241,6 +244,34 @@ static uint64_t point_hits(const grid_t* g, int dim, const double* q, const doub
 
 /* --------------------------------------------------------------- pattern */
 
+/* One pattern row: the ascending j >= i with dist2(c_i, c_j) < lim. */
+static uint64_t pattern_row(const grid_t* g, int dim, const double* centres, uint64_t i, double lim,
+                            uint32_t** row, uint64_t* cap) {
+    const double* ci = centres + i * dim;
+    uint64_t k = 0;
+    GRID_FOR_CANDIDATES(g, ci, j, {
+        if (j >= i && dist2(dim, ci, centres + (uint64_t)j * dim) < lim) {
+            if (k == *cap) {
+                *cap *= 2;
+                *row = (uint32_t*)realloc(*row, *cap * sizeof(uint32_t));
+            }
+            (*row)[k++] = j;
+        }
+    });
+    for (uint64_t a = 1; a < k; ++a) { /* insertion sort (rows are short) */
+        uint32_t t = (*row)[a];
+        uint64_t b = a;
+        while (b > 0 && (*row)[b - 1] > t) {
+            (*row)[b] = (*row)[b - 1];
+            --b;
+        }
+        (*row)[b] = t;
+    }
+    return k;
+}
+
+/* Rows are independent: counted in parallel, prefix-summed, then filled in
+ * parallel (the result does not depend on the thread count). */
 int orc_pattern(int dim, const double* centres, uint64_t m, double alpha, uint64_t* row_ptr,
                 uint32_t* cols) {
     if ((dim != 2 && dim != 3) || m == 0 || !(alpha > 0.0) || !isfinite(alpha))
@@ -250,35 +281,30 @@ int orc_pattern(int dim, const double* centres, uint64_t m, double alpha, uint64
     const double lim = two_r * two_r;
     grid_t g;
     if (grid_build(&g, dim, centres, m, two_r) != ORC_OK) return ORC_RUNTIME;
-    uint64_t cap = 256;
-    uint32_t* row = (uint32_t*)malloc(cap * sizeof(uint32_t));
     row_ptr[0] = 0;
-    for (uint64_t i = 0; i < m; ++i) {
-        const double* ci = centres + i * dim;
-        uint64_t k = 0;
-        GRID_FOR_CANDIDATES(&g, ci, j, {
-            if (j >= i && dist2(dim, ci, centres + (uint64_t)j * dim) < lim) {
-                if (k == cap) {
-                    cap *= 2;
-                    row = (uint32_t*)realloc(row, cap * sizeof(uint32_t));
-                }
-                row[k++] = j;
-            }
-        });
-        /* insertion sort (rows are short) */
-        for (uint64_t a = 1; a < k; ++a) {
-            uint32_t t = row[a];
-            uint64_t b = a;
-            while (b > 0 && row[b - 1] > t) {
-                row[b] = row[b - 1];
-                --b;
-            }
-            row[b] = t;
-        }
-        if (cols) memcpy(cols + row_ptr[i], row, k * sizeof(uint32_t));
-        row_ptr[i + 1] = row_ptr[i] + k;
+#pragma omp parallel
+    {
+        uint64_t cap = 256;
+        uint32_t* row = (uint32_t*)malloc(cap * sizeof(uint32_t));
+#pragma omp for schedule(dynamic, 512)
+        for (int64_t i = 0; i < (int64_t)m; ++i)
+            row_ptr[i + 1] = pattern_row(&g, dim, centres, (uint64_t)i, lim, &row, &cap);
+        free(row);
     }
-    free(row);
+    for (uint64_t i = 0; i < m; ++i) row_ptr[i + 1] += row_ptr[i];
+    if (cols) {
+#pragma omp parallel
+        {
+            uint64_t cap = 256;
+            uint32_t* row = (uint32_t*)malloc(cap * sizeof(uint32_t));
+#pragma omp for schedule(dynamic, 512)
+            for (int64_t i = 0; i < (int64_t)m; ++i) {
+                const uint64_t k = pattern_row(&g, dim, centres, (uint64_t)i, lim, &row, &cap);
+                memcpy(cols + row_ptr[i], row, k * sizeof(uint32_t));
+            }
+            free(row);
+        }
+    }
     grid_free(&g);
     return ORC_OK;
 }
@@ -298,6 +324,19 @@ static int64_t find_slot(const uint64_t* row_ptr, const uint32_t* cols, uint32_t
 
 /* -------------------------------------------------------------- assembly */
 
+/* Parallel without changing a single bit: points are processed in chunks;
+ * first every point's sorted hit list is computed (parallel over points),
+ * then the output rows are partitioned among threads and each thread walks
+ * the chunk's points in ascending order, applying only the updates of its
+ * own rows.  Every entry therefore receives exactly the sequential
+ * (point-ascending) addition sequence of coo.cpp:80 / coo.cpp:144. */
+#define ORC_CHUNK (1u << 20)
+
+typedef struct {
+    hit_t* buf;
+    uint64_t len, cap;
+} hitbuf_t;
+
 int orc_assemble(int dim, const double* pts, const double* h, uint64_t n, const double* centres,
                  uint64_t m, int family, double alpha, const uint64_t* row_ptr,
                  const uint32_t* cols, double* vals, double* rhs, uint64_t* hits) {
@@ -311,29 +350,87 @@ int orc_assemble(int dim, const double* pts, const double* h, uint64_t n, const 
     const double r2 = radius * radius; /* kdtree.cpp:64 */
     grid_t g;
     if (grid_build(&g, dim, centres, m, radius) != ORC_OK) return ORC_RUNTIME;
-    uint64_t cap = 256;
-    hit_t* hb = (hit_t*)malloc(cap * sizeof(hit_t));
+    const uint64_t chunk = n < ORC_CHUNK ? (n ? n : 1) : ORC_CHUNK;
+    const hit_t** plist = (const hit_t**)malloc(chunk * sizeof(hit_t*));
+    uint32_t* pk = (uint32_t*)malloc(chunk * sizeof(uint32_t));
+    uint64_t* poff = (uint64_t*)malloc(chunk * sizeof(uint64_t));
+    int* pthr = (int*)malloc(chunk * sizeof(int));
+    int nthr = 1;
+#ifdef _OPENMP
+    nthr = omp_get_max_threads();
+#endif
+    hitbuf_t* tb = (hitbuf_t*)calloc((size_t)nthr, sizeof(hitbuf_t));
     int status = ORC_OK;
-    for (uint64_t p = 0; p < n && status == ORC_OK; ++p) {
-        const uint64_t k =
-            point_hits(&g, dim, pts + p * dim, centres, family, alpha, r2, &hb, &cap);
-        const double hp = h[p];
-        for (uint64_t a = 0; a < k; ++a) {
-            const uint32_t ca = hb[a].id;
-            const double va = hb[a].v;
-            hits[ca]++;
-            rhs[ca] += va * hp; /* coo.cpp:80 */
-            for (uint64_t b = a; b < k; ++b) {
-                const int64_t s = find_slot(row_ptr, cols, ca, hb[b].id);
-                if (s < 0) {
-                    status = ORC_RUNTIME;
-                    break;
+    const int64_t nparts = (int64_t)nthr * 8;
+    for (uint64_t c0 = 0; c0 < n && status == ORC_OK; c0 += chunk) {
+        const uint64_t cn = n - c0 < chunk ? n - c0 : chunk;
+#pragma omp parallel
+        {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            hitbuf_t* B = &tb[tid];
+            B->len = 0;
+            uint64_t cap = 256;
+            hit_t* hb = (hit_t*)malloc(cap * sizeof(hit_t));
+#pragma omp for schedule(static)
+            for (int64_t q = 0; q < (int64_t)cn; ++q) {
+                const uint64_t p = c0 + (uint64_t)q;
+                const uint64_t k = point_hits(&g, dim, pts + p * dim, centres, family, alpha, r2, &hb, &cap);
+                if (B->len + k > B->cap) {
+                    B->cap = (B->len + k) * 2 + 1024;
+                    B->buf = (hit_t*)realloc(B->buf, B->cap * sizeof(hit_t));
                 }
-                vals[s] += va * hb[b].v; /* coo.cpp:144 */
+                memcpy(B->buf + B->len, hb, k * sizeof(hit_t));
+                poff[q] = B->len;
+                pthr[q] = tid;
+                pk[q] = (uint32_t)k;
+                B->len += k;
+            }
+            free(hb);
+        }
+        for (uint64_t q = 0; q < cn; ++q) plist[q] = tb[pthr[q]].buf + poff[q];
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t part = 0; part < nparts; ++part) {
+            const uint32_t r0 = (uint32_t)((uint64_t)part * m / (uint64_t)nparts);
+            const uint32_t r1 = (uint32_t)((uint64_t)(part + 1) * m / (uint64_t)nparts);
+            if (r0 == r1) continue;
+            for (uint64_t q = 0; q < cn; ++q) {
+                const hit_t* hl = plist[q];
+                const uint64_t k = pk[q];
+                if (k == 0 || hl[k - 1].id < r0 || hl[0].id >= r1) continue;
+                uint64_t a = 0, hi = k; /* first hit with id >= r0 */
+                while (a < hi) {
+                    const uint64_t mid = (a + hi) >> 1;
+                    if (hl[mid].id < r0) a = mid + 1;
+                    else hi = mid;
+                }
+                const double hp = h[c0 + q];
+                for (; a < k && hl[a].id < r1; ++a) {
+                    const uint32_t ca = hl[a].id;
+                    const double va = hl[a].v;
+                    hits[ca]++;
+                    rhs[ca] += va * hp; /* coo.cpp:80 */
+                    for (uint64_t b2 = a; b2 < k; ++b2) {
+                        const int64_t s = find_slot(row_ptr, cols, ca, hl[b2].id);
+                        if (s < 0) {
+#pragma omp atomic write
+                            status = ORC_RUNTIME;
+                            break;
+                        }
+                        vals[s] += va * hl[b2].v; /* coo.cpp:144 */
+                    }
+                }
             }
         }
     }
-    free(hb);
+    for (int t = 0; t < nthr; ++t) free(tb[t].buf);
+    free(tb);
+    free(plist);
+    free(pk);
+    free(poff);
+    free(pthr);
     grid_free(&g);
     return status;
 }
@@ -349,15 +446,19 @@ int orc_evaluate(int dim, const double* centres, uint64_t m, const double* w, in
     const double r2 = radius * radius;
     grid_t g;
     if (grid_build(&g, dim, centres, m, radius) != ORC_OK) return ORC_RUNTIME;
-    uint64_t cap = 256;
-    hit_t* hb = (hit_t*)malloc(cap * sizeof(hit_t));
-    for (uint64_t i = 0; i < nq; ++i) {
-        const uint64_t k = point_hits(&g, dim, q + i * dim, centres, family, alpha, r2, &hb, &cap);
-        double acc = 0.0;
-        for (uint64_t a = 0; a < k; ++a) acc += w[hb[a].id] * hb[a].v; /* model.cpp:63-64 */
-        f[i] = acc;
+#pragma omp parallel
+    {
+        uint64_t cap = 256;
+        hit_t* hb = (hit_t*)malloc(cap * sizeof(hit_t));
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < (int64_t)nq; ++i) {
+            const uint64_t k = point_hits(&g, dim, q + (uint64_t)i * dim, centres, family, alpha, r2, &hb, &cap);
+            double acc = 0.0;
+            for (uint64_t a = 0; a < k; ++a) acc += w[hb[a].id] * hb[a].v; /* model.cpp:63-64 */
+            f[i] = acc;
+        }
+        free(hb);
     }
-    free(hb);
     grid_free(&g);
     return ORC_OK;
 }

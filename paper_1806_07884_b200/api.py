@@ -188,6 +188,13 @@ class Engine:
         self._check(self._L.rbg_system_device(self._ctx, C.byref(ptr), C.byref(cnt)))
         return int(ptr.value), int(cnt.value)
 
+    def hits(self) -> tuple[np.ndarray, int]:
+        """Per-centre hit counts and design_nnz of the last assembly (no values copied)."""
+        hits = np.empty(self.m)
+        dn = C.c_uint64()
+        self._check(self._L.rbg_get_system(self._ctx, None, None, _p(hits), C.byref(dn)))
+        return hits, int(dn.value)
+
     def system(self) -> dict:
         info = self.pattern_info()
         vals = np.empty(info["nnz_upper"])
@@ -356,11 +363,11 @@ def fit(points, values, refs, kernel: KernelSpec, tol: float = 0.0, max_iter: in
     eng.set_centres(r, kernel)
     eng.set_poly(poly)
     eng.assemble(pts, h)
-    sysd = eng.system()
+    hits, design_nnz = eng.hits()
     c, diag = eng.solve(tol, max_iter)
     a = eng.poly_solution() if poly else None
-    rep.design_nnz = sysd["design_nnz"]
-    rep.empty_support_refs = np.flatnonzero(sysd["hits"] == 0).tolist()
+    rep.design_nnz = design_nnz
+    rep.empty_support_refs = np.flatnonzero(hits == 0).tolist()
     rep.ridge_lambda = diag["ridge_lambda"]
     rep.ridge_shift = diag["ridge_shift"]
     rep.iterations = diag["iterations"]

@@ -120,6 +120,9 @@ rbg_status rbg_create(int device, rbg_ctx** out) {
         RBG_CUDA(cudaEventCreate(&ctx->ev0));
         RBG_CUDA(cudaEventCreate(&ctx->ev1));
         for (auto& e : ctx->ev_asm) RBG_CUDA(cudaEventCreate(&e));
+        // [0] pattern misses, [1] scratch (first_nonfinite), [2..7] diagnostics
+        ctx->counters.reserve(8);
+        RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 8 * sizeof(unsigned long long), ctx->stream));
     });
     if (s != RBG_OK) {
         // keep the message reachable through a static buffer

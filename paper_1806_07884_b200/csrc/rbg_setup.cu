@@ -470,7 +470,7 @@ void setup_pattern(rbg_ctx* ctx) {
 
     // ---- system + point workspace sized for this centre set ----------------
     ctx->sys.reserve(ctx->nnz_upper + 2 * m + 4 * m + 20);  // room for the polynomial border
-    ctx->counters.reserve(4);
+    // counters: allocated (8) by rbg_create
     RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
     RBG_CUDA(cudaStreamSynchronize(st));
     ctx->have_pattern = true;
