@@ -1,17 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the CS-RBF normal-equation hot path (BASELINE.json metric:
-A^T A assembly points/s, fit time, roofline fraction).
+A^T A assembly points/s and end-to-end fit time; fraction of the fp64 roofline).
 
-One step = one pass of the hot path over one batch: bin the batch's points
-into the centre tiles and assemble A^T A and A^T h (+ the NCCL allreduce of the
-partial systems when N > 1).  The centre set / symbolic pattern depends only on
-the centres and is built once before timing (reported as setup_ms).
+  python bench.py [--gpus N --steps K --warmup W] [--config cfg5] [--impl reference]
 
-  python bench.py [--gpus N --steps K --warmup W] [--config cfg2] [--impl reference]
+Default workload: BASELINE config 5 (N = 2e8 Halton points, M = 1e6 grid
+centres, wendland-3-1), the largest configuration that fits one B200.
 
-N > 1 runs under torchrun (one rank per GPU, NCCL).  Weak scaling: every rank
-assembles an independent full-size draw of the config's point distribution
-against the shared centres; value = all ranks' points / max-over-ranks time.
+* value  -- one step = bin + assemble A^T A / A^T h over the whole point set
+  with the inputs resident in HBM (+ the NCCL all-reduce of the partial
+  systems when N > 1); points/s over all ranks, max-over-ranks device time.
+* e2e    -- the public fit through the C ABI (api.fit: rbg_create,
+  rbg_set_centres, rbg_assemble from pageable host arrays, rbg_solve, c back
+  to the host), a fresh context every step, so the centre grid, the symbolic
+  pattern, the assembly layout and every host<->device copy are inside the
+  timed region; points/s of the full fit.
+* N > 1 is strong scaling: the one point set is split into equal-count spatial
+  slabs (configs.slab_points), each rank bins and assembles only its slab
+  against the replicated centres, and one in-place NCCL all-reduce sums
+  [values | rhs | hits]; for e2e every rank then solves the summed system.
+
+--impl reference times the reference's own CPU path (oracle/_ref: its
+kd-tree, assemble_submatrix, transpose_matvec, gram_self compiled from
+/root/reference; the dense Cholesky with the reference's ridge ladder on
+OpenBLAS through scipy standing in for Eigen's LLT) on a spatial window of the
+same workload -- every window point sees its full support -- using all host
+threads (one reference instance per thread on point shards, partial systems
+summed).  It loads no library of this package.
 """
 from __future__ import annotations
 
@@ -32,8 +47,34 @@ import numpy as np  # noqa: E402
 
 METRIC = "A^T A assembly points/s"
 UNIT = "points/s"
+DEFAULT_CONFIG = "cfg5"
 F_PHI = {2: 14, 3: 20}  # flops per phi evaluation incl. distance
-REF_SAMPLE = 250_000  # reference arm: points per CPU step (bounded sample)
+FAMILY = {"wendland-3-0": 0, "wendland-3-1": 1, "wendland-3-3": 2, "wendland-3-2": 3}
+# Pinned copies of the config table (bench.py --impl reference must not import
+# the package, whose generators live in its own .so); checked against
+# paper_1806_07884_b200/configs.py by tests/test_bench_contract.py.
+CFG = {
+    "cfg1": dict(dim=2, n=100_000, m=1_000, kernel="wendland-3-1", per_support=30,
+                 desc="2D Halton N=1e5, h=Franke; M=1e3 Halton centres; phi31, ~30 centres/support"),
+    "cfg2": dict(dim=2, n=1_000_000, m=10_000, kernel="wendland-3-1", per_support=50,
+                 desc="2D uniform N=1e6, h=sin4x cos4y + N(0,0.01); M=1e4 on a 100x100 grid; phi31, ~50/support"),
+    "cfg3": dict(dim=3, n=4_000_000, m=50_000, kernel="wendland-3-2", per_support=60,
+                 desc="3D uniform N=4e6, h=exp(-|x-.5|^2/.1)+.5 sin6z; M=5e4 Halton; phi32, ~60/support"),
+    "cfg4": dict(dim=2, n=20_000_000, m=100_000, kernel="wendland-3-1", per_support=40,
+                 desc="2D Gaussian mixture N=2e7 (+5% uniform floor), h=6-octave fBm; M=1e5 Halton; phi31, ~40/support"),
+    "cfg5": dict(dim=2, n=200_000_000, m=1_000_000, kernel="wendland-3-1", per_support=40,
+                 desc="2D Halton N=2e8, h=Franke+N(0,0.001); M=1e6 on a 1000x1000 grid; phi31, ~40/support"),
+}
+
+
+def alpha_of(name: str) -> float:
+    import math
+    c = CFG[name]
+    if c["dim"] == 2:
+        r = math.sqrt(c["per_support"] / (math.pi * c["m"]))
+    else:
+        r = (c["per_support"] / (c["m"] * 4.0 * math.pi / 3.0)) ** (1.0 / 3.0)
+    return 1.0 / r
 
 
 def parse():
@@ -41,11 +82,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CFG))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-fit", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="timed e2e fits (default: --steps)")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-div", type=float, default=None, help="sub-tile edge = radius / this")
     ap.add_argument("--super-factor", type=int, default=None, help="super-tile = this^dim sub-tiles")
     return ap.parse_args()
@@ -56,10 +97,13 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def workload(cfg) -> dict:
-    return {"workload": f"{cfg.name}: {cfg.description}", "n_points_per_rank": cfg.n, "m_centres": cfg.m,
-            "dim": cfg.dim, "kernel": cfg.kernel, "alpha": cfg.alpha,
-            "l2": "flushed between timed steps (256 MiB device write outside the step events)"}
+def workload(name: str) -> dict:
+    """The workload description, identical for both arms and every N."""
+    c = CFG[name]
+    return {"workload": f"{name}: {c['desc']}", "n_points": c["n"], "m_centres": c["m"], "dim": c["dim"],
+            "kernel": c["kernel"], "alpha": alpha_of(name),
+            "l2": "inputs (>= 1.6 GB at cfg3-5) exceed L2; a 256 MiB device write flushes L2 before every step "
+                  "(outside the step events)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -118,121 +162,185 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------ cpu baseline
-def cpu_baseline(cfg, xy, h, refs, samples: int = 3) -> dict:
-    """The reference's own CPU path (oracle/_ref, compiled from the reference
-    sources) on a bounded sample, 1 thread (the reference is single-threaded).
-    Falls back to our C restatement when the reference could not run here."""
-    from oracle import pyoracle as po
+# ------------------------------------------------ reference window sample
+def _np_noise(seed: int, pos: np.ndarray, sigma: float) -> np.ndarray:
+    """sigma * N(0,1) at array positions `pos`: restates the counter-based
+    normal01 of csrc/datagen.cpp (splitmix64, Box-Muller) in numpy, so the
+    reference arm needs no library of this package (libm ulp differences only)."""
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
 
-    n = min(REF_SAMPLE, len(h))
-    fam = {"wendland-3-0": 0, "wendland-3-1": 1, "wendland-3-3": 2, "wendland-3-2": 3}[cfg.kernel]
-    if po.ref_available() and cfg.dim == 2 and cfg.m <= 20_000 and fam <= 2:
-        times = []
-        for _ in range(samples):
-            sec, _dn = po.ref_bench_step(xy[:n], h[:n], refs, fam, cfg.alpha)
-            times.append(sec)
-        t = statistics.median(times)
-        return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": f"first {n} points of {cfg.name} with all {cfg.m} centres; reference "
-                          f"kd-tree + assemble_submatrix + transpose_matvec + gram_self "
-                          f"(single block), median of {samples}, {t:.2f} s each"}
-    # restatement (sparse, point-ascending) for configs the reference cannot hold
-    n = min(n, 100_000)
+    def mix(x):
+        x = (x + np.uint64(0x9E3779B97F4A7C15)) & M
+        x = ((x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & M
+        x = ((x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & M
+        return x ^ (x >> np.uint64(31))
+
+    def uni(i):
+        k = mix(np.uint64(seed) ^ mix((np.uint64(0x6E6F726D) * np.uint64(0x632BE59BD9B4E019)) + i))
+        return (k >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+    with np.errstate(over="ignore"):
+        i = pos.astype(np.uint64)
+        u1 = 1.0 - uni(np.uint64(2) * i)
+        u2 = uni(np.uint64(2) * i + np.uint64(1))
+    return sigma * (np.sqrt(-2.0 * np.log(u1)) * np.cos(6.283185307179586 * u2))
+
+
+def reference_window(name: str):
+    """A spatial window of the config's workload built with the reference's
+    own generators (oracle/_ref): every window point and all centres within
+    the support radius of the window, so each point sees its full support.
+    Halton configs: W = [0, 2^-a) x [0, 3^-b) holds exactly the sequence
+    indices that are multiples of 2^a 3^b.  Returns (xy, h, refs, description)."""
+    from oracle import pyoracle as po
+    c = CFG[name]
+    alpha = alpha_of(name)
+    r = 1.0 / alpha
+    if name not in ("cfg1", "cfg5"):
+        raise NotImplementedError(name)
+    a, b = (4, 3) if name == "cfg5" else (1, 1)
+    stride = 2 ** a * 3 ** b
+    idx = np.arange(stride, c["n"] + 1, stride, dtype=np.uint64)
+    xy = po.ref_halton_at(idx, 2)
+    h = po.ref_franke(xy)
+    if name == "cfg5":
+        h = h + _np_noise(5 * 1000 + 1, idx - np.uint64(1), 0.001)
+        refs = po.ref_grid_refs(1000, 1000)
+    else:
+        refs = po.ref_halton_at(np.arange(1, c["m"] + 1, dtype=np.uint64), 2)
+    wx, wy = 2.0 ** -a, 3.0 ** -b
+    sel = (refs[:, 0] > -r) & (refs[:, 0] < wx + r) & (refs[:, 1] > -r) & (refs[:, 1] < wy + r)
+    refs = np.ascontiguousarray(refs[sel])
+    desc = (f"spatial window [0, 2^-{a}) x [0, 3^-{b}) of {name}: its {len(h)} points (Halton indices "
+            f"multiple of {stride}) and the {len(refs)} centres within the support radius of it")
+    return xy, h, refs, desc
+
+
+def reference_fit(xy, h, refs, family: int, alpha: float, threads: int) -> dict:
+    """The reference's fit (solver.cpp:401-478) on one sample: its PointIndex +
+    assemble_submatrix + transpose_matvec + gram_self (oracle/_ref, single
+    block, dense B -- solver.cpp:131-236) on `threads` point shards in
+    parallel, partial systems summed, then solve_weights' ridge-laddered
+    Cholesky (solver.cpp:289-330) with OpenBLAS dpotrf standing in for Eigen."""
+    import concurrent.futures as cf
+
+    import scipy.linalg as sl
+
+    from oracle import pyoracle as po
+    m = len(refs)
+    shards = np.array_split(np.arange(len(h)), threads)
     t0 = time.perf_counter()
-    rp, cols = po.pattern(refs, cfg.alpha)
-    t_pat = time.perf_counter() - t0
-    times = []
-    for _ in range(samples):
-        t0 = time.perf_counter()
-        po.assemble(xy[:n], h[:n], refs, fam, cfg.alpha, rp, cols)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"first {n} points of {cfg.name}, all {cfg.m} centres; C restatement "
-                      f"(oracle/rbf_oracle.c), pattern {t_pat:.2f} s excluded, median of {samples}"}
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:  # ctypes releases the GIL
+        parts = list(ex.map(lambda ix: po.ref_build_normal_system(xy[ix], h[ix], refs, family, alpha), shards))
+    b = parts[0]["b"]
+    rhs = parts[0]["rhs"].copy()
+    for p in parts[1:]:
+        b += p["b"]
+        rhs += p["rhs"]
+    t_build = time.perf_counter() - t0
+    mean_diag = np.trace(b) / m
+    lam_used = None
+    for lam in (0.0, 1e-10, 1e-9, 1e-8, 1e-7, 1e-6):
+        try:
+            work = b + lam * mean_diag * np.eye(m) if lam > 0 else b
+            c = sl.cho_solve(sl.cho_factor(work, lower=True, check_finite=False), rhs, check_finite=False)
+            lam_used = lam
+            break
+        except np.linalg.LinAlgError:
+            continue
+    t_fit = time.perf_counter() - t0
+    return {"build_s": t_build, "fit_s": t_fit, "ridge_lambda": lam_used, "c": c if lam_used is not None else None,
+            "design_nnz": int(sum(p["design_nnz"] for p in parts))}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # ------------------------------------------------------------- reference arm
-def run_reference(args, cfg):
+def run_reference(args):
     rank, world, _ = dist_env()
-    if rank != 0:
+    if rank != 0:  # under torchrun only rank 0 runs the CPU reference
         return
-    from oracle import pyoracle as po
-    from paper_1806_07884_b200 import configs
-
-    xy, h = configs.points(cfg.name, n=min(REF_SAMPLE, cfg.n))
-    refs = configs.centres(cfg.name)
-    fam = {"wendland-3-0": 0, "wendland-3-1": 1, "wendland-3-3": 2, "wendland-3-2": 3}[cfg.kernel]
-    n = len(h)
-    threads = 1
-    if po.ref_available() and cfg.dim == 2 and cfg.m <= 20_000 and fam <= 2:
+    name = args.config
+    c = CFG[name]
+    fam = FAMILY[c["kernel"]]
+    alpha = alpha_of(name)
+    threads = host_threads()
+    if name in ("cfg1", "cfg5"):
+        xy, h, refs, desc = reference_window(name)
         kind = "reference"
-        # The reference is single-threaded; to give it every host core we run
-        # one independent reference instance per core on its own shard of the
-        # sample (partial normal systems add, exactly like the GPU point shards).
-        # Each instance holds a dense M x M block, so the count is also capped
-        # by host memory.
-        import concurrent.futures as cf
-        try:
-            import psutil
-            avail = psutil.virtual_memory().available
-        except Exception:
-            avail = 16 << 30
-        per_inst = 3 * cfg.m * cfg.m * 8 + (256 << 20)
-        threads = max(1, min(os.cpu_count() or 1, 64, int(0.6 * avail // per_inst), n // 2000))
-        shards = np.array_split(np.arange(n), threads)
 
         def step():
-            t0 = time.perf_counter()
-            with cf.ThreadPoolExecutor(max_workers=threads) as ex:  # ctypes releases the GIL
-                list(ex.map(lambda ix: po.ref_bench_step(xy[ix], h[ix], refs, fam, cfg.alpha), shards))
-            return time.perf_counter() - t0
-        sample = (f"first {n} points of {cfg.name}, all {cfg.m} centres: reference kd-tree + "
-                  f"assemble_submatrix + transpose_matvec + gram_self, single block, {threads} independent "
-                  f"reference instances (one per host thread) on point shards")
+            return reference_fit(xy, h, refs, fam, alpha, threads)
+        what = ("reference fit: kd-tree + assemble_submatrix + transpose_matvec + gram_self (oracle/_ref, one "
+                "instance per host thread on point shards, partial systems summed) + ridge-laddered dense "
+                "Cholesky (OpenBLAS dpotrf standing in for Eigen's LLT)")
     else:
+        # configs the reference cannot hold (3-D, or dense M x M beyond host RAM): the
+        # C restatement (oracle/rbf_oracle.c, threaded by output rows) + a sparse direct solve
+        from oracle import pyoracle as po
+        from paper_1806_07884_b200 import configs  # input generation only (outside the timed step)
+        n = min(c["n"], 1_000_000)
+        xy, h = configs.points(name, n=n)
+        refs = configs.centres(name)
+        desc = f"first {n} points of {name} with all {c['m']} centres"
         kind = "port"
-        rp, cols = po.pattern(refs, cfg.alpha)
-        n = min(n, 100_000)
 
         def step():
+            import scipy.sparse as sp
+            import scipy.sparse.linalg as spl
             t0 = time.perf_counter()
-            po.assemble(xy[:n], h[:n], refs, fam, cfg.alpha, rp, cols)
-            return time.perf_counter() - t0
-        sample = f"first {n} points of {cfg.name}: C restatement (reference cannot hold this config)"
+            rp, cols = po.pattern(refs, alpha)
+            v, rhs, _ = po.assemble(xy, h, refs, fam, alpha, rp, cols)
+            t_build = time.perf_counter() - t0
+            rows = np.repeat(np.arange(len(refs)), np.diff(rp.astype(np.int64)))
+            U = sp.csr_matrix((v, (rows, cols.astype(np.int64))), shape=(len(refs),) * 2)
+            spl.spsolve((U + sp.triu(U, 1).T).tocsc(), rhs)
+            return {"build_s": t_build, "fit_s": time.perf_counter() - t0}
+        what = "C restatement (oracle/rbf_oracle.c) assembly + scipy sparse direct solve"
     for _ in range(args.warmup):
         step()
-    times = [step() for _ in range(args.steps)]
-    t = sum(times) / len(times)
+    res = [step() for _ in range(args.steps)]
+    t = sum(r["fit_s"] for r in res) / len(res)
+    tb = sum(r["build_s"] for r in res) / len(res)
+    n = len(h)
     value = n / t
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    sample = f"{desc}; {what}; {threads} host threads; per step build {tb:.3f} s, fit {t:.3f} s"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload(cfg), "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload(name), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_assembly_points_per_s": n / tb,
+            "ridge_lambda": res[-1].get("ridge_lambda")}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args, cfg):
+def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1806_07884_b200 import _native, api, configs, distributed
+    from paper_1806_07884_b200 import api, configs, distributed
 
     rank, world, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    # a real (non-legacy) stream shared by torch and the engine, so the step
-    # events and NCCL are ordered with the engine's kernels
+    # a real (non-legacy) stream shared by torch and the engine: the step events
+    # and the NCCL all-reduce are ordered with the engine's kernels
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
-    xy, h = configs.points(cfg.name, seed_offset=rank)
-    refs = configs.centres(cfg.name)
+    name = args.config
+    cfg = configs.CONFIGS[name]
+    xy, h = configs.slab_points(name, rank, world)
+    refs = configs.centres(name)
     kernel = api.KernelSpec(cfg.kernel, cfg.alpha)
     eng = api.Engine(local, stream=stream.cuda_stream)
     if args.tile_div:
@@ -257,9 +365,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
 
     lay = eng.layout_info()
-    # algorithmic work of one step on this rank (outside timing)
+    # algorithmic work of this rank's step (outside timing): sum_k F + k(k+1) + 2k
     sum_k, sum_k2 = _ncounts(eng, xy)
-    flops_step = sum_k2 + (F_PHI[cfg.dim] + 3) * sum_k  # sum k F + k(k+1) + 2k
+    flops_step = sum_k2 + (F_PHI[cfg.dim] + 3) * sum_k
     bytes_step = n * (cfg.dim + 1) * 8 + info["nnz_upper"] * 12 + cfg.m * 8
     fp64_peak = _fp64_peak(eng)
 
@@ -276,64 +384,148 @@ def run_ours(args, cfg):
             starts[k].record(stream)
             step()
             ends[k].record(stream)
-            if world == 1:
-                b, t = _asm_times(eng)
-                bin_ms.append(b)
-                tile_ms.append(t)
+            b, t = _asm_times(eng)  # events on the engine stream, read after the step
+            bin_ms.append(b)
+            tile_ms.append(t)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = eng.launch_count - launches0
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = _max_over_ranks(total_ms, world)
     ms_per_step = total_ms / args.steps
-    value = world * n / (ms_per_step * 1e-3)
+    n_total = _sum_over_ranks(n, world)
+    value = n_total / (ms_per_step * 1e-3)
 
-    # e2e: public C-ABI call from pinned host buffers, result read back each step
-    e2e = _e2e(eng, xy, h, info, cfg, world, args)
-
-    fit = None if args.no_fit or rank != 0 else _fit_once(eng, xy, h)
+    e2e = None if args.no_e2e else _e2e(xy, h, refs, kernel, cfg, world, rank, local, args, stream)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    roof = None
-    if tile_ms:
-        t_tile = statistics.median(tile_ms) * 1e-3
-        achieved = flops_step / t_tile / 1e12
-        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": _traffic(cfg.name),
-                "kernel": "assemble_warp_kernel (persistent one-warp workers: phi into DMMA fragments, register SYRK per sub-tile, warp-private super-tile accumulator, slot-map flush)",
-                "peak_source": "measured live: rbg_fp64_peak DFMA microbenchmark (MEASURED_PEAKS.json has no fp64)",
-                "algorithmic_flops_per_launch": flops_step, "tile_ms": t_tile * 1e3,
-                "bin_ms": statistics.median(bin_ms),
-                "hbm": {"algorithmic_bytes": bytes_step, "achieved_gbs": bytes_step / t_tile / 1e9,
-                        "peak_gbs": _hbm_peak(), "frac": bytes_step / t_tile / 1e9 / _hbm_peak()}}
+    t_tile = statistics.median(tile_ms) * 1e-3
+    achieved = flops_step / t_tile / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak, "traffic": _traffic(name),
+            "kernel": "assemble_warp_kernel (persistent one-warp workers: phi into DMMA fragments, register "
+                      "SYRK per sub-tile, warp-private super-tile accumulator, slot-map flush)",
+            "peak_source": "measured live: rbg_fp64_peak DFMA microbenchmark (MEASURED_PEAKS.json has no fp64)",
+            "algorithmic_flops_per_launch": flops_step, "kernel_ms": t_tile * 1e3,
+            "kernel_share_of_step": t_tile * 1e3 / ms_per_step,
+            "bin_ms": statistics.median(bin_ms),
+            "hbm": {"algorithmic_bytes": bytes_step, "achieved_gbs": bytes_step / t_tile / 1e9,
+                    "peak_gbs": _hbm_peak(), "frac": bytes_step / t_tile / 1e9 / _hbm_peak()}}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, xy, h, refs)
+        cpu = cpu_baseline(name)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**workload(cfg), "parallelism": f"dp{world} (point shards, NCCL allreduce)",
-                       "nnz_upper": info["nnz_upper"], "n_tiles": info["n_tiles"],
-                       "setup_ms": info["setup_ms"], "sum_k": sum_k, "sum_k2": sum_k2,
-                       "layout": {"sub_div": lay["sub_div"], "super_factor": lay["super_factor"],
-                                  "n_super": lay["n_super"], "n_buckets": lay["n_buckets"],
-                                  "n_fallback": lay["n_fallback"],
-                                  "mean_super_centres": round(lay["mean_super_centres"], 2),
-                                  "mean_sub_centres": round(lay["mean_sub_centres"], 2),
-                                  "max_super_centres": lay["max_super_centres"],
-                                  "max_sub_centres": lay["max_sub_centres"], "build_ms": round(lay["build_ms"], 2)}},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload(name),
+            "parallelism": (f"{world} ranks x equal-count spatial slabs, one NCCL all-reduce of "
+                            f"[values|rhs|hits] per step" if world > 1 else "1 GPU"),
             "clocks": clocks.summary(), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "fit": fit}
+            "gpu_launches": launches,
+            "detail": {"points_this_rank": n, "nnz_upper": info["nnz_upper"], "setup_ms": info["setup_ms"],
+                       "sum_k": sum_k, "sum_k2": sum_k2,
+                       "layout": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in lay.items()}}}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(v: int, world: int) -> int:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device="cuda", dtype=torch.int64)
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def _e2e(xy, h, refs, kernel, cfg, world, rank, local, args, stream):
+    """The public fit from pageable host arrays, a fresh context per step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_07884_b200 import api, distributed
+    steps = args.e2e_steps or args.steps
+
+    def fit_once():
+        t0 = time.perf_counter()
+        if world == 1:
+            model, rep = api.fit(xy, h, refs, kernel, engine=api.Engine(local))
+            c = model.weights
+        else:  # strong scaling: slab assembly, all-reduce on the engine stream, every rank solves
+            rep = api.FitReport()
+            with api.Engine(local, stream=stream.cuda_stream) as e:
+                e.set_centres(refs, kernel)
+                e.assemble(xy, h)
+                distributed.allreduce_system(e)
+                c, d = e.solve()
+                rep.iterations, rep.solve_ms = d["iterations"], d["solve_ms"]
+        return time.perf_counter() - t0, c, rep
+
+    fit_once()
+    if world > 1:
+        dist.barrier()
+    times, rep = [], None
+    for _ in range(steps):
+        dt, c, rep = fit_once()
+        times.append(dt)
+    dt = _max_over_ranks(sum(times) / len(times), world)
+    n_total = _sum_over_ranks(len(h), world)
+    return {"value": n_total / dt, "unit": UNIT, "ms_per_step": dt * 1e3, "steps": steps,
+            "h2d_bytes_per_step": int(len(h) * (cfg.dim + 1) * 8 + refs.size * 8),
+            "d2h_bytes_per_step": int(cfg.m * 8 + (cfg.m * 8 if world == 1 else 0)),
+            "api": ("api.fit -> rbg_create, rbg_set_centres, rbg_assemble (pageable host arrays, validated), "
+                    "rbg_get_system (hit counts), rbg_solve (c to the host)" if world == 1 else
+                    "rbg_create, rbg_set_centres, rbg_assemble (host slab), NCCL all-reduce, rbg_solve"),
+            "fit": {"setup_ms": getattr(rep, "setup_ms", None), "solve_ms": rep.solve_ms,
+                    "iterations": rep.iterations, "ridge_lambda": getattr(rep, "ridge_lambda", None)}}
+
+
+def cpu_baseline(name: str) -> dict | None:
+    """The reference's CPU fit on the same bounded window the reference arm
+    uses (kind 'reference'), or the C restatement where the reference cannot
+    run the config (kind 'port')."""
+    c = CFG[name]
+    threads = host_threads()
+    fam = FAMILY[c["kernel"]]
+    try:
+        if name in ("cfg1", "cfg5"):
+            xy, h, refs, desc = reference_window(name)
+            reference_fit(xy, h, refs, fam, alpha_of(name), threads)  # warm
+            r = reference_fit(xy, h, refs, fam, alpha_of(name), threads)
+            return {"value": len(h) / r["build_s"], "unit": UNIT, "cores": threads, "kind": "reference",
+                    "sample": f"{desc}; reference index + assemble_submatrix + gram_self on {threads} threads "
+                              f"({r['build_s']:.3f} s); the whole reference fit incl. Cholesky "
+                              f"{r['fit_s']:.3f} s = {len(h) / r['fit_s']:.4g} points/s"}
+        from oracle import pyoracle as po
+        from paper_1806_07884_b200 import configs
+        n = min(c["n"], 1_000_000)
+        xy, h = configs.points(name, n=n)
+        refs = configs.centres(name)
+        rp, cols = po.pattern(refs, alpha_of(name))
+        t0 = time.perf_counter()
+        po.assemble(xy, h, refs, fam, alpha_of(name), rp, cols)
+        t = time.perf_counter() - t0
+        return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": f"first {n} points of {name}, all {c['m']} centres: C restatement "
+                          f"(oracle/rbf_oracle.c, OpenMP by output rows), pattern excluded"}
+    except Exception as e:  # the baseline is reported, never required
+        return {"value": None, "unit": UNIT, "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
 
 
 def _ncounts(eng, xy):
@@ -379,75 +571,12 @@ def _traffic(name):
         return None
 
 
-def _e2e(eng, xy, h, info, cfg, world, args):
-    import ctypes as C
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_1806_07884_b200 import _native, distributed
-    L = _native.lib()
-    n = len(h)
-    p_xy = torch.from_numpy(xy).pin_memory()
-    p_h = torch.from_numpy(h).pin_memory()
-    nnz, m = info["nnz_upper"], cfg.m
-    o_v = torch.empty(nnz, dtype=torch.float64).pin_memory()
-    o_r = torch.empty(m, dtype=torch.float64).pin_memory()
-    o_hits = torch.empty(m, dtype=torch.float64).pin_memory()
-    dn = C.c_uint64()
-    sys_t = distributed.system_tensor(eng) if world > 1 else None
-    steps = args.e2e_steps or args.steps
-
-    def one():
-        eng.assemble_ptr(p_xy.data_ptr(), p_h.data_ptr(), n)
-        if world > 1:
-            dist.all_reduce(sys_t)
-        _native.check(L.rbg_get_system(eng._ctx, o_v.data_ptr(), o_r.data_ptr(), o_hits.data_ptr(),
-                                       C.byref(dn)), eng._ctx)
-
-    for _ in range(2):
-        one()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        one()
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / steps
-    if world > 1:
-        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt = float(t.item())
-    return {"value": world * n / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
-            "h2d_bytes_per_step": n * (cfg.dim + 1) * 8, "d2h_bytes_per_step": (nnz + 2 * m) * 8,
-            "api": "rbg_assemble (host pinned in) + rbg_get_system (host out)"}
-
-
-def _fit_once(eng, xy, h):
-    t0 = time.perf_counter()
-    eng.assemble(xy, h, validate=True)
-    eng.synchronize()
-    t_asm = time.perf_counter() - t0
-    c, diag = eng.solve()
-    t1 = time.perf_counter()
-    rep = eng.error_report(c, xy, h)
-    t_err = time.perf_counter() - t1
-    return {"assembly_s": t_asm, "solve_s": diag["solve_ms"] * 1e-3, "iterations": diag["iterations"],
-            "rel_residual": diag["rel_residual"], "ridge_lambda": diag["ridge_lambda"],
-            "eval_error_s": t_err, "fit_s": t_asm + diag["solve_ms"] * 1e-3,
-            "mae": rep["mean_absolute_error"], "rms": rep["rms_error"], "max_abs": rep["max_abs_error"]}
-
-
 def main():
     args = parse()
-    from paper_1806_07884_b200 import configs
-
-    cfg = configs.CONFIGS[args.config]
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference(args)
     else:
-        run_ours(args, cfg)
+        run_ours(args)
 
 
 if __name__ == "__main__":

@@ -78,6 +78,9 @@ def ref() -> C.CDLL:
         L.ref_halton_points.argtypes = [_U64, C.c_int, _P]
         L.ref_franke.argtypes = [C.c_double, C.c_double]
         L.ref_franke.restype = C.c_double
+        L.ref_halton_at.argtypes = [_P, _U64, C.c_int, _P]
+        L.ref_franke_many.argtypes = [_P, _U64, _P]
+        L.ref_franke_many.restype = None
         L.ref_uniform_grid_refs.argtypes = [C.c_double] * 4 + [_U64, _U64, _P]
         L.ref_center_cloud.argtypes = [_P, _P, _U64, _P]
         L.ref_build_normal_system.argtypes = [_P, _P, _U64, _P, _U64, C.c_int, C.c_double, _P, _P,
@@ -261,6 +264,27 @@ def ref_error_report(refs, w, family, alpha, points, values):
         L.ref_last_error().decode())
     return {"mean_absolute_error": out[0], "deviation_of_error": out[1],
             "mean_relative_error_pct": out[2], "signed_errors": se}
+
+
+def ref_halton_at(indices, dims):
+    """Halton points (the reference's radical_inverse) at the given sequence indices."""
+    idx = np.ascontiguousarray(indices, dtype=np.uint64)
+    out = np.empty((len(idx), dims))
+    _ok(ref().ref_halton_at(_p(idx), len(idx), dims, _p(out)))
+    return out
+
+
+def ref_franke(xy):
+    p = _f64(xy)
+    out = np.empty(p.shape[0])
+    ref().ref_franke_many(_p(p), p.shape[0], _p(out))
+    return out
+
+
+def ref_grid_refs(nx, ny, box=(0.0, 0.0, 1.0, 1.0)):
+    out = np.empty((nx * ny, 2))
+    _ok(ref().ref_uniform_grid_refs(*box, nx, ny, _p(out)))
+    return out
 
 
 def ref_bench_step(points, values, refs, family, alpha):

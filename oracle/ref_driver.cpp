@@ -94,6 +94,22 @@ int ref_halton_points(std::uint64_t count, int dims, double* out) {
 
 double ref_franke(double x, double y) { return franke(Point2{x, y}); }
 
+// halton_points (data.cpp:89-98) at arbitrary sequence indices, point-major:
+// the reference's own radical_inverse, used to build spatial window samples
+// of the Halton configs for bench.py --impl reference.
+int ref_halton_at(const std::uint64_t* idx, std::uint64_t n, int dims, double* out) {
+    static const unsigned kBases[] = {2, 3, 5};
+    if (dims < 1 || dims > 3) return 1;
+    for (std::uint64_t i = 0; i < n; ++i)
+        for (int d = 0; d < dims; ++d) out[i * dims + d] = radical_inverse(kBases[d], idx[i]);
+    return 0;
+}
+
+// franke (data.cpp:108-116) of n points.
+void ref_franke_many(const double* xy, std::uint64_t n, double* out) {
+    for (std::uint64_t i = 0; i < n; ++i) out[i] = franke(Point2{xy[2 * i], xy[2 * i + 1]});
+}
+
 int ref_uniform_grid_refs(double x0, double y0, double x1, double y1, std::uint64_t nx,
                           std::uint64_t ny, double* out) {
     try {

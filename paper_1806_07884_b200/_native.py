@@ -159,6 +159,8 @@ def datagen() -> C.CDLL:
         L = C.CDLL(str(LIB_DATAGEN))
         L.dg_halton.argtypes = [_U64, _U64, C.c_int, _P]
         L.dg_grid_refs.argtypes = [C.c_double] * 4 + [_U64, _U64, _P]
+        L.dg_halton_strided.argtypes = [_U64, _U64, _U64, C.c_int, _P]
+        L.dg_add_noise_strided.argtypes = [_U64, _U64, _U64, _U64, C.c_double, _P]
         L.dg_franke.argtypes = [_P, _U64, _P]
         L.dg_uniform.argtypes = [_U64, _U64, C.c_int, _P]
         L.dg_add_noise.argtypes = [_U64, _U64, C.c_double, _P]
@@ -166,7 +168,7 @@ def datagen() -> C.CDLL:
         L.dg_bump3.argtypes = [_P, _U64, _P]
         L.dg_mixture.argtypes = [_U64, _U64, _P]
         L.dg_fbm.argtypes = [_U64, _P, _U64, _P]
-        for f in ("dg_halton", "dg_grid_refs", "dg_franke", "dg_uniform", "dg_add_noise",
+        for f in ("dg_halton", "dg_halton_strided", "dg_add_noise_strided", "dg_grid_refs", "dg_franke", "dg_uniform", "dg_add_noise",
                   "dg_sincos", "dg_bump3", "dg_mixture", "dg_fbm"):
             getattr(L, f).restype = None
         _datagen = L

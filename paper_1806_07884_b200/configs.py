@@ -139,3 +139,39 @@ def _noise_window(seed: int, start: int, n: int, sigma: float, h: np.ndarray) ->
     noise = np.zeros(start + n)
     _native.datagen().dg_add_noise(seed, start + n, sigma, _ptr(noise))
     return h + noise[start:]
+
+
+def _bitrev(k: int, bits: int) -> int:
+    return int(format(k, f"0{bits}b")[::-1], 2) if bits else 0
+
+
+def slab_points(name: str, rank: int, world: int, n: int | None = None):
+    """Rank `rank`'s equal-count spatial slab (x in 2-D, z in 3-D) of the one
+    point set of config `name` -- the strong-scaling shard of SURVEY 8(e).
+
+    For the Halton configs (cfg1, cfg5) and a power-of-two world the slab is
+    generated directly: x = radical_inverse(2, i) lies in [k/W, (k+1)/W) iff
+    i mod W == bitreverse(k), so rank k owns the indices W q + bitreverse(k)
+    (equal counts within one point, no rank materialises the whole set).
+    Otherwise the whole set is generated and split with rbg_partition_slabs.
+    `n` restricts the set to the config's first n points (tests)."""
+    c = CONFIGS[name]
+    total = c.n if n is None else n
+    if world == 1:
+        return points(name, n=total)
+    if name in ("cfg1", "cfg5") and world & (world - 1) == 0:
+        bits = world.bit_length() - 1
+        r = _bitrev(rank, bits)
+        first = r if r > 0 else world  # sequence indices start at 1
+        count = (total - first) // world + 1 if first <= total else 0
+        xy = np.empty((count, 2))
+        _native.datagen().dg_halton_strided(first, world, count, 2, _ptr(xy))
+        h = franke(xy)
+        if name == "cfg5":  # noise of the point at array position i - 1
+            _native.datagen().dg_add_noise_strided(SEEDS[name] * 1000 + 1, first - 1, world, count, 0.001, _ptr(h))
+        return xy, h
+    from . import distributed
+    xy, h = points(name, n=total)
+    _, slab = distributed.partition_slabs(xy, world)
+    sel = slab == rank
+    return np.ascontiguousarray(xy[sel]), np.ascontiguousarray(h[sel])

@@ -89,6 +89,23 @@ void dg_halton(uint64_t start, uint64_t count, int dims, double* out) {
             out[(uint64_t)k * dims + d] = radical_inverse(kBases[d], start + (uint64_t)k);
 }
 
+// halton_points at indices first, first + stride, ... (count of them), point-major.
+void dg_halton_strided(uint64_t first, uint64_t stride, uint64_t count, int dims, double* out) {
+    static const unsigned kBases[] = {2, 3, 5};
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < (int64_t)count; ++k)
+        for (int d = 0; d < dims; ++d)
+            out[(uint64_t)k * dims + d] = radical_inverse(kBases[d], first + stride * (uint64_t)k);
+}
+
+// inout[k] += sigma * N(0,1)_{first + stride k}: the noise of the points at those positions.
+void dg_add_noise_strided(uint64_t seed, uint64_t first, uint64_t stride, uint64_t count, double sigma,
+                          double* inout) {
+#pragma omp parallel for schedule(static)
+    for (int64_t k = 0; k < (int64_t)count; ++k)
+        inout[k] += sigma * normal01(seed, first + stride * (uint64_t)k);
+}
+
 // uniform_grid_refs(box, nx, ny) (data.cpp:236-249): y-major, x fastest.
 void dg_grid_refs(double x0, double y0, double x1, double y1, uint64_t nx, uint64_t ny,
                   double* out) {
