@@ -175,3 +175,21 @@ def slab_points(name: str, rank: int, world: int, n: int | None = None):
     _, slab = distributed.partition_slabs(xy, world)
     sel = slab == rank
     return np.ascontiguousarray(xy[sel]), np.ascontiguousarray(h[sel])
+
+
+def window_points(name: str, a: int, b: int):
+    """The points of a Halton config (cfg1, cfg5) inside the spatial window
+    [0, 2^-a) x [0, 3^-b): exactly the sequence indices that are multiples of
+    2^a 3^b (radical_inverse(2, i) < 2^-a iff 2^a | i, same for base 3), at
+    the config's full density.  Returns (xy, h)."""
+    if name not in ("cfg1", "cfg5"):
+        raise KeyError(name)
+    c = CONFIGS[name]
+    stride = (2 ** a) * (3 ** b)
+    count = c.n // stride
+    xy = np.empty((count, 2))
+    _native.datagen().dg_halton_strided(stride, stride, count, 2, _ptr(xy))
+    h = franke(xy)
+    if name == "cfg5":
+        _native.datagen().dg_add_noise_strided(SEEDS[name] * 1000 + 1, stride - 1, stride, count, 0.001, _ptr(h))
+    return xy, h

@@ -45,12 +45,14 @@ int main(int argc, char** argv) {
     b.values.assign(all.values.begin() + half, all.values.end());
     const KernelSpec kernel(KernelFamily::wendland_3_1, alpha);
 
+    std::fprintf(stderr, "read %llu points, %llu refs\n", (unsigned long long)n, (unsigned long long)m);
     Device dev_b(0);  // "rank 1": its partial system stays on the device
     build_normal_system(b, refs, kernel, false, nullptr, &dev_b);
     double* other = nullptr;
     std::uint64_t other_count = 0;
     if (rbg_system_device(dev_b.ctx(), &other, &other_count) != RBG_OK) return 3;
 
+    std::fprintf(stderr, "rank-1 partial built\n");
     Device dev_a(0);
     cudaStream_t mine;
     cudaStreamCreateWithFlags(&mine, cudaStreamNonBlocking);
@@ -63,6 +65,7 @@ int main(int argc, char** argv) {
     };
     const NormalSystem two = build_normal_system(a, refs, kernel, false, nullptr, &dev_a, hook);
 
+    std::fprintf(stderr, "hooked build done\n");
     Device dev_c(0);
     const NormalSystem one = build_normal_system(all, refs, kernel, false, nullptr, &dev_c);
     double worst = 0.0, scale = 0.0;
