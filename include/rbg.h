@@ -134,6 +134,18 @@ typedef struct {
 rbg_status rbg_solve(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out,
                      rbg_solve_diag* diag);
 
+/* Orthogonal least-squares re-pass (least_squares_repass, solver.cpp:345-397),
+ * the reference's last resort when the normal equations are numerically
+ * singular (fit, solver.cpp:439-464): 4096-row chunks of the augmented design
+ * [A P | h] of the n points (host arrays, AoS) through an incremental
+ * Householder QR on the device, then R w = R[:, width].  w_out receives the
+ * m (+ T with the polynomial border) unknowns; *ok = 0 when w is not finite
+ * (rank-deficient design: the caller keeps the ridge solution).  Limited to
+ * m + T <= rbg_repass_max_unknowns() (RBG_INVALID_ARGUMENT beyond). */
+rbg_status rbg_least_squares_repass(rbg_ctx* ctx, const double* points, const double* h, uint64_t n,
+                                    double* w_out, int* ok);
+uint64_t rbg_repass_max_unknowns(void);
+
 /* ---- evaluation -------------------------------------------------------------
  * Replaces evaluate_model / evaluate_shifted (model.cpp:50-72,192-194) with a
  * zero offset: f_q = sum_j c_j phi(|q - xi_j|) over the

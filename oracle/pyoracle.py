@@ -266,6 +266,25 @@ def ref_error_report(refs, w, family, alpha, points, values):
             "mean_relative_error_pct": out[2], "signed_errors": se}
 
 
+def ref_dense_design(points, refs, family, alpha):
+    """Dense design matrix A (n x m) from the reference's own assemble_submatrix
+    (coo.cpp:166-192): A[p, j] = phi(|p - ref_j|) inside the strict support."""
+    p, r = _f64(points), _f64(refs)
+    n, m = p.shape[0], r.shape[0]
+    cap = n * m
+    rows = np.empty(cap, dtype=np.uint32)
+    cols = np.empty(cap, dtype=np.uint32)
+    vals = np.empty(cap)
+    nnz = _U64()
+    L = ref()
+    _ok(L.ref_assemble_triplets(_p(p), n, _p(r), m, family, alpha, cap, _p(rows), _p(cols), _p(vals),
+                                C.byref(nnz)), L.ref_last_error().decode())
+    k = nnz.value
+    a = np.zeros((n, m))
+    a[rows[:k], cols[:k]] = vals[:k]
+    return a
+
+
 def ref_halton_at(indices, dims):
     """Halton points (the reference's radical_inverse) at the given sequence indices."""
     idx = np.ascontiguousarray(indices, dtype=np.uint64)

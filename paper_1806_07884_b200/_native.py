@@ -101,6 +101,8 @@ _SIGS = {
     "rbg_set_system": (C.c_int, [_P, _P, _P, _P]),
     "rbg_solve": (C.c_int, [_P, C.POINTER(SolveOptions), _P, C.POINTER(SolveDiag)]),
     "rbg_evaluate": (C.c_int, [_P, _P, _P, _U64, _P]),
+    "rbg_least_squares_repass": (C.c_int, [_P, _P, _P, _U64, _P, C.POINTER(C.c_int)]),
+    "rbg_repass_max_unknowns": (_U64, []),
     "rbg_evaluate_device": (C.c_int, [_P, _P, _P, _U64, _P]),
     "rbg_error_report": (C.c_int, [_P, _P, _P, _P, _U64, C.POINTER(ErrorStats), _P]),
     "rbg_partition_slabs": (C.c_int, [C.c_int, _P, _U64, C.c_int, C.c_int, _P, _P]),

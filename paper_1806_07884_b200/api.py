@@ -248,6 +248,15 @@ class Engine:
         self._check(self._L.rbg_solve(self._ctx, C.byref(opts), _p(c), C.byref(diag)))
         return c, {k: getattr(diag, k) for k, _ in diag._fields_}
 
+    def least_squares_repass(self, points, values):
+        """least_squares_repass (solver.cpp:345-397) on the device: the weights
+        (m, then the border terms with poly) or None when they are not finite."""
+        pts, h = _f64(points, self.dim), _f64(values)
+        w = np.empty(self.m + self.poly_terms)
+        ok = C.c_int()
+        self._check(self._L.rbg_least_squares_repass(self._ctx, _p(pts), _p(h), h.shape[0], _p(w), C.byref(ok)))
+        return w if ok.value else None
+
     def evaluate(self, c, queries) -> np.ndarray:
         cc = _f64(c)
         q = _f64(queries, self.dim)
@@ -364,19 +373,43 @@ def fit(points, values, refs, kernel: KernelSpec, tol: float = 0.0, max_iter: in
     eng.set_poly(poly)
     eng.assemble(pts, h)
     hits, design_nnz = eng.hits()
-    c, diag = eng.solve(tol, max_iter)
-    a = eng.poly_solution() if poly else None
     rep.design_nnz = design_nnz
     rep.empty_support_refs = np.flatnonzero(hits == 0).tolist()
+    rep.setup_ms = eng.pattern_info()["setup_ms"]
+    m, T = r.shape[0], eng.poly_terms
+    try:
+        c, diag = eng.solve(tol, max_iter)
+        a = eng.poly_solution() if poly else None
+    except _native.RuntimeFailure:
+        # solver.cpp:439-451: even the deepest ridge rung failed; the re-pass is
+        # the last resort and a rank-deficient design rethrows
+        if m + T > _native.lib().rbg_repass_max_unknowns():
+            raise
+        w = eng.least_squares_repass(pts, h)
+        if w is None:
+            raise
+        c, a = w[:m], (w[m:] if poly else None)
+        diag = {"ridge_lambda": 0.0, "ridge_shift": 0.0, "iterations": 0, "rel_residual": 0.0, "solve_ms": 0.0}
+        rep.warnings.append("normal equations unsolvable; weights recovered by an orthogonal re-pass "
+                            "over the data")
     rep.ridge_lambda = diag["ridge_lambda"]
     rep.ridge_shift = diag["ridge_shift"]
     rep.iterations = diag["iterations"]
     rep.rel_residual = diag["rel_residual"]
     rep.solve_ms = diag["solve_ms"]
-    rep.setup_ms = eng.pattern_info()["setup_ms"]
-    if rep.ridge_lambda > 0.0:
-        rep.warnings.append("normal equations numerically singular; ridge solution kept (the "
-                            "orthogonal re-pass is not available on the GPU path)")
+    if rep.ridge_lambda > 0.0:  # solver.cpp:452-464
+        if m + T > _native.lib().rbg_repass_max_unknowns():
+            raise _native.RuntimeFailure(
+                _native.RBG_RUNTIME_ERROR,
+                f"normal equations numerically singular (ridge lambda {rep.ridge_lambda:g}); the orthogonal "
+                f"re-pass (solver.cpp:345-397) is limited to {_native.lib().rbg_repass_max_unknowns()} "
+                f"unknowns on the GPU path")
+        w = eng.least_squares_repass(pts, h)
+        if w is not None:
+            c, a = w[:m], (w[m:] if poly else None)
+            rep.ridge_lambda = rep.ridge_shift = 0.0
+            rep.warnings.append("normal equations numerically singular; weights recovered by an orthogonal "
+                                "re-pass over the data")
     return Model(kernel, r, c, poly=a), rep
 
 

@@ -280,12 +280,48 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     std::vector<double> c(m);
     rbg_solve_options so{options.tol, options.max_iter};
     rbg_solve_diag d{};
-    check(rbg_solve(ctx, &so, c.data(), &d), ctx);
     std::optional<std::array<double, 3>> poly;
-    if (options.poly) {
-        std::array<double, 4> a{};
-        check(rbg_get_poly_solution(ctx, a.data()), ctx);
-        poly = std::array<double, 3>{a[0], a[1], a[2]};
+    const std::size_t unknowns = m + (options.poly ? 3 : 0);
+    // the orthogonal re-pass over the data (solver.cpp:345-397); false: not finite
+    const auto repass = [&]() -> bool {
+        std::vector<double> w(unknowns);
+        int ok = 0;
+        check(rbg_least_squares_repass(ctx, flat(cloud.points), cloud.values.data(), cloud.size(), w.data(), &ok),
+              ctx);
+        if (!ok) return false;
+        std::copy(w.begin(), w.begin() + static_cast<std::ptrdiff_t>(m), c.begin());
+        if (options.poly) poly = std::array<double, 3>{w[m], w[m + 1], w[m + 2]};
+        return true;
+    };
+    const rbg_status st = rbg_solve(ctx, &so, c.data(), &d);
+    if (st == RBG_RUNTIME_ERROR && unknowns <= rbg_repass_max_unknowns()) {
+        // solver.cpp:439-451: every ridge rung failed; a rank-deficient design rethrows
+        const std::string why = rbg_last_error(ctx);
+        if (!repass()) throw std::runtime_error(why);
+        d = rbg_solve_diag{};
+        local.warnings.push_back(
+            "normal equations unsolvable; weights recovered by an orthogonal re-pass over the data");
+    } else {
+        check(st, ctx);
+        if (options.poly) {
+            std::array<double, 4> a{};
+            check(rbg_get_poly_solution(ctx, a.data()), ctx);
+            poly = std::array<double, 3>{a[0], a[1], a[2]};
+        }
+    }
+    if (d.ridge_lambda > 0.0) {  // solver.cpp:452-464
+        if (unknowns > rbg_repass_max_unknowns())
+            throw std::runtime_error("normal equations numerically singular (ridge lambda " +
+                                     std::to_string(d.ridge_lambda) +
+                                     "); the orthogonal re-pass (solver.cpp:345-397) is limited to " +
+                                     std::to_string(rbg_repass_max_unknowns()) + " unknowns on the GPU path");
+        if (repass()) {
+            d.ridge_lambda = 0.0;
+            d.ridge_shift = 0.0;
+            local.warnings.push_back(
+                "normal equations numerically singular; weights recovered by an orthogonal re-pass over "
+                "the data");
+        }
     }
     local.gram_solve_seconds = seconds_since(t0);
     local.design_nnz = design_nnz;
@@ -294,10 +330,6 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     local.ridge_lambda = d.ridge_lambda;
     local.ridge_shift = d.ridge_shift;
     local.iterations = d.iterations;
-    if (d.ridge_lambda > 0.0)
-        local.warnings.push_back(
-            "normal equations numerically singular; ridge solution kept (the orthogonal "
-            "re-pass is not implemented on the GPU path)");
     rbg_pattern_info info{};
     check(rbg_get_pattern_info(ctx, &info), ctx);
     local.peak_bytes = (info.nnz_upper + 2 * m) * sizeof(double);

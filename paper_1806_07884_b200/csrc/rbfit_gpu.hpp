@@ -12,8 +12,9 @@
 //  * the block planner (BlockPlan / ram budget) has no GPU meaning: the whole
 //    pattern is resident; FitReport::plan reports one block;
 //  * the linear-polynomial border (FitOptions::poly) is supported (2-D: P =
-//    [x, y, 1] as the reference); the orthogonal re-pass is not implemented
-//    on the GPU path (FitReport warning).
+//    [x, y, 1] as the reference); the orthogonal re-pass of fit
+//    (solver.cpp:345-397, 439-464) runs on the GPU up to 4096 unknowns and
+//    fit throws beyond that instead of keeping a ridge-biased solution.
 #pragma once
 
 #include <array>

@@ -389,6 +389,30 @@ rbg_status rbg_solve(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out,
     });
 }
 
+uint64_t rbg_repass_max_unknowns(void) { return rbg::repass_max_refs(); }
+
+rbg_status rbg_least_squares_repass(rbg_ctx* ctx, const double* points, const double* h, uint64_t n,
+                                    double* w_out, int* ok) {
+    return guarded(ctx, [&] {
+        require_centres(ctx);
+        if (n == 0 || !points || !h || !w_out || !ok) throw Error(RBG_INVALID_ARGUMENT, "null or empty input");
+        const uint64_t unknowns = ctx->m + (uint64_t)ctx->pterms();
+        if (unknowns > rbg::repass_max_refs())
+            throw Error(RBG_INVALID_ARGUMENT, "least-squares re-pass: " + std::to_string(unknowns) +
+                                                  " unknowns exceed the GPU path's limit of " +
+                                                  std::to_string(rbg::repass_max_refs()));
+        bind(ctx);
+        const int dim = ctx->dim;
+        ctx->in_pts.reserve(n * dim);
+        ctx->in_h.reserve(n);
+        rbg::h2d(ctx, ctx->in_pts.p, points, n * dim * sizeof(double));
+        rbg::h2d(ctx, ctx->in_h.p, h, n * sizeof(double));
+        if (const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, dim); bad < n)
+            throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
+        *ok = rbg::least_squares_repass(ctx, ctx->in_pts.p, ctx->in_h.p, n, w_out) ? 1 : 0;
+    });
+}
+
 rbg_status rbg_evaluate_device(rbg_ctx* ctx, const double* d_c, const double* d_q, uint64_t nq,
                                double* d_f) {
     return guarded(ctx, [&] {

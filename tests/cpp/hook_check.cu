@@ -81,6 +81,7 @@ int main(int argc, char** argv) {
     const bool same_empty = one.empty_support_refs == two.empty_support_refs;
     std::printf("hook calls=%d bad_stream=%d |dB|=%.3g |drhs|=%.3g empty_same=%d\n", calls, bad_stream,
                 worst / scale, wr / sr, (int)same_empty);
+    dev_a.set_stream(nullptr);  // the context must not outlive the caller's stream on it
     cudaStreamDestroy(mine);
     return (calls == 1 && bad_stream == 0 && worst / scale < 1e-12 && wr / sr < 1e-12 && same_empty) ? 0 : 1;
 }

@@ -102,3 +102,29 @@ def test_allreduce_hook_runs_on_the_context_stream(tmp_path):
         refs.tofile(f)
     r = subprocess.run([str(exe), str(inp)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_host_layer_flat_kernel_fit_takes_the_repass(exe, tmp_path):
+    """rbfit_b200::fit on test_solver.cpp:282-312's flat-kernel case: the
+    warnings name the re-pass, ridge is 0 and the MAE is the least-squares
+    one (within 2 %, LAPACK lstsq on the reference's dense design)."""
+    from oracle import pyoracle as po
+    xy = po.ref_halton_at(np.arange(1, 9001, dtype=np.uint64), 2)
+    h = po.ref_franke(xy)
+    refs = po.ref_grid_refs(9, 9)
+    inp = tmp_path / "in.bin"
+    with open(inp, "wb") as f:
+        np.array([len(h), len(refs)], dtype=np.uint64).tofile(f)
+        np.array([0.25]).tofile(f)
+        xy.tofile(f)
+        h.tofile(f)
+        refs.tofile(f)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), "flat", str(inp), str(out)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    mae, ridge = np.fromfile(out, dtype=np.float64)
+    a = po.ref_dense_design(xy, refs, 2, 0.25)
+    w = np.linalg.lstsq(a, h, rcond=None)[0]
+    assert ridge == 0.0
+    assert mae == pytest.approx(float(np.mean(np.abs(a @ w - h))), rel=0.02)
