@@ -139,6 +139,8 @@ rbg_status rbg_destroy(rbg_ctx* ctx) {
     if (!ctx) return RBG_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+    rbg::RecycleScope recycle;  // the streams are drained: the work buffers go to the device cache
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     for (auto& e : ctx->ev_asm)

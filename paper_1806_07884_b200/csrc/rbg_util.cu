@@ -2,6 +2,8 @@
 // the binning (counting sort) and symbolic (pattern) phases.
 #include <algorithm>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -179,11 +181,170 @@ void segmented_sort_u32(rbg_ctx* ctx, uint32_t* keys, const uint64_t* seg_ptr, u
 }
 
 
+// ------------------------------------------------------- device memory cache
+namespace {
+
+struct CachedBlock {
+    int device;
+    size_t bytes;
+    void* p;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+thread_local int g_recycle_depth = 0;
+
+void trim_cache(int device) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (auto it = g_cache.begin(); it != g_cache.end();) {
+        if (it->device == device) {
+            cudaFree(it->p);
+            it = g_cache.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+}  // namespace
+
+RecycleScope::RecycleScope() { ++g_recycle_depth; }
+RecycleScope::~RecycleScope() { --g_recycle_depth; }
+
+void* dev_alloc(size_t bytes, size_t* got) {
+    int device = 0;
+    RBG_CUDA(cudaGetDevice(&device));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        size_t best = ~size_t{0};
+        size_t bi = 0;
+        for (size_t i = 0; i < g_cache.size(); ++i) {
+            const CachedBlock& c = g_cache[i];
+            if (c.device == device && c.bytes >= bytes && c.bytes <= 2 * bytes + (size_t{2} << 20) && c.bytes < best) {
+                best = c.bytes;
+                bi = i;
+            }
+        }
+        if (best != ~size_t{0}) {
+            void* p = g_cache[bi].p;
+            *got = g_cache[bi].bytes;
+            g_cache.erase(g_cache.begin() + (std::ptrdiff_t)bi);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+        cudaGetLastError();
+        trim_cache(device);
+        e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess)
+        throw Error(RBG_CUDA_ERROR, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    *got = bytes;
+    return p;
+}
+
+void dev_free(void* p, size_t bytes) {
+    if (!p) return;
+    if (g_recycle_depth > 0 && bytes >= (size_t{1} << 20)) {
+        int device = 0;
+        if (cudaGetDevice(&device) == cudaSuccess) {
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            g_cache.push_back({device, bytes, p});
+            return;
+        }
+    }
+    cudaFree(p);
+}
+
 // ------------------------------------------------------- staged host copies
+// Pageable host memory cannot be DMA'd directly: chunks are copied into a
+// process-wide ring of pinned buffers by a persistent pool of host threads
+// while the copy engine drains the previous chunks.
 namespace {
 
 constexpr size_t kStageBytes = size_t{64} << 20;
+constexpr int kStageBufs = 4;
 constexpr size_t kDirectBytes = size_t{16} << 20;
+
+class CopyPool {
+  public:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        nthreads_ = std::max(1u, std::min(16u, hw ? hw : 1u));
+        for (unsigned t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { run(t); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    // memcpy split over every pool thread (the caller takes part 0)
+    void copy(void* dst, const void* src, size_t bytes) {
+        std::unique_lock<std::mutex> lk(mu_);
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        bytes_ = bytes;
+        pending_ = nthreads_ - 1;
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        part(0);
+        lk.lock();
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void part(unsigned t) {
+        const size_t per = (bytes_ + nthreads_ - 1) / nthreads_;
+        const size_t off = std::min(bytes_, (size_t)t * per), len = std::min(per, bytes_ - off);
+        if (len) std::memcpy(dst_ + off, src_ + off, len);
+    }
+    void run(unsigned t) {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            lk.unlock();
+            part(t);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    unsigned nthreads_ = 1;
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    bool stop_ = false;
+    uint64_t gen_ = 0;
+    unsigned pending_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+struct Staging {
+    std::mutex mu;  // one staged copy at a time per process
+    void* buf[kStageBufs] = {};
+    cudaEvent_t ev[kStageBufs] = {};
+    CopyPool* pool = nullptr;
+    void ensure() {
+        if (!pool) pool = new CopyPool();  // never destroyed: threads outlive static teardown order
+        for (int b = 0; b < kStageBufs; ++b) {
+            if (!buf[b]) RBG_CUDA(cudaHostAlloc(&buf[b], kStageBytes, cudaHostAllocPortable));
+            if (!ev[b]) RBG_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+        }
+    }
+};
+Staging& staging() {
+    static Staging* s = new Staging();
+    return *s;
+}
 
 }  // namespace
 
@@ -196,49 +357,26 @@ bool page_locked(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-namespace {
-
-void ensure_staging(rbg_ctx* ctx) {
-    for (int b = 0; b < 2; ++b) {
-        if (!ctx->pin[b]) RBG_CUDA(cudaHostAlloc(&ctx->pin[b], kStageBytes, cudaHostAllocPortable));
-        if (!ctx->pin_ev[b]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->pin_ev[b], cudaEventDisableTiming));
-    }
-}
-
-void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-    const size_t per = (bytes + hw - 1) / hw;
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < hw && t * per < bytes; ++t)
-        th.emplace_back([=] {
-            std::memcpy(static_cast<char*>(dst) + t * per, static_cast<const char*>(src) + t * per,
-                        std::min(per, bytes - t * per));
-        });
-    std::memcpy(dst, src, std::min(per, bytes));
-    for (auto& x : th) x.join();
-}
-
-}  // namespace
-
 void h2d(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
     cudaStream_t st = ctx->stream;
     if (bytes < kDirectBytes || page_locked(src)) {
         RBG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         return;
     }
-    ensure_staging(ctx);
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.ensure();
     size_t off = 0;
     for (int i = 0; off < bytes; ++i) {
-        const int b = i & 1;
+        const int b = i % kStageBufs;
         const size_t len = std::min(kStageBytes, bytes - off);
-        RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[b]));  // the copy that last read this buffer is done
-        parallel_memcpy(ctx->pin[b], static_cast<const char*>(src) + off, len);
-        RBG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->pin[b], len, cudaMemcpyHostToDevice, st));
-        RBG_CUDA(cudaEventRecord(ctx->pin_ev[b], st));
+        RBG_CUDA(cudaEventSynchronize(S.ev[b]));  // the copy that last read this buffer is done
+        S.pool->copy(S.buf[b], static_cast<const char*>(src) + off, len);
+        RBG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, S.buf[b], len, cudaMemcpyHostToDevice, st));
+        RBG_CUDA(cudaEventRecord(S.ev[b], st));
         off += len;
     }
-    RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[0]));
-    RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[1]));
+    for (int b = 0; b < kStageBufs; ++b) RBG_CUDA(cudaEventSynchronize(S.ev[b]));
 }
 
 void d2h(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
@@ -248,30 +386,26 @@ void d2h(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
         RBG_CUDA(cudaStreamSynchronize(st));
         return;
     }
-    ensure_staging(ctx);
+    Staging& S = staging();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.ensure();
     const size_t n_chunks = (bytes + kStageBytes - 1) / kStageBytes;
     auto issue = [&](size_t i) {
         const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
-        RBG_CUDA(cudaMemcpyAsync(ctx->pin[i & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, st));
-        RBG_CUDA(cudaEventRecord(ctx->pin_ev[i & 1], st));
+        RBG_CUDA(cudaMemcpyAsync(S.buf[i % kStageBufs], static_cast<const char*>(src) + off, len,
+                                 cudaMemcpyDeviceToHost, st));
+        RBG_CUDA(cudaEventRecord(S.ev[i % kStageBufs], st));
     };
-    issue(0);
+    for (size_t i = 0; i < std::min<size_t>(n_chunks, kStageBufs - 1); ++i) issue(i);
     for (size_t i = 0; i < n_chunks; ++i) {
-        RBG_CUDA(cudaEventSynchronize(ctx->pin_ev[i & 1]));
-        if (i + 1 < n_chunks) issue(i + 1);  // the next chunk lands while this one drains
+        RBG_CUDA(cudaEventSynchronize(S.ev[i % kStageBufs]));
+        if (i + kStageBufs - 1 < n_chunks) issue(i + kStageBufs - 1);  // later chunks land while this one drains
         const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
-        parallel_memcpy(static_cast<char*>(dst) + off, ctx->pin[i & 1], len);
+        S.pool->copy(static_cast<char*>(dst) + off, S.buf[i % kStageBufs], len);
     }
 }
 
-void release_staging(rbg_ctx* ctx) {
-    for (int b = 0; b < 2; ++b) {
-        if (ctx->pin[b]) cudaFreeHost(ctx->pin[b]);
-        if (ctx->pin_ev[b]) cudaEventDestroy(ctx->pin_ev[b]);
-        ctx->pin[b] = nullptr;
-        ctx->pin_ev[b] = nullptr;
-    }
-}
+void release_staging(rbg_ctx*) {}  // the ring is process-wide
 
 namespace {
 __global__ void first_nonfinite_kernel(const double* __restrict__ p, uint64_t n, int dim,
