@@ -7,6 +7,8 @@
 #include <vector>
 
 #include <cstdlib>
+#include <exception>
+#include <thread>
 
 #include "rbg_internal.cuh"
 
@@ -39,18 +41,22 @@ void require_centres(const rbg_ctx* ctx) {
     if (!ctx->have_centres)
         throw Error(RBG_NOT_READY, "no reference points set (call rbg_set_centres first)");
 }
-// The symbolic pattern (K2) is built at the first call that needs it.
+// The symbolic pattern (K2) is built at the first call that needs it, after
+// the tile grid (rbg::ensure_grid); the system buffer is sized for it.
 void require_pattern(rbg_ctx* ctx) {
     require_centres(ctx);
-    if (ctx->have_pattern) return;
     RBG_CUDA(cudaSetDevice(ctx->device));
-    RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-    rbg::setup_pattern(ctx);
-    RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-    RBG_CUDA(cudaEventSynchronize(ctx->ev1));
-    float ms = 0.f;
-    RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-    ctx->setup_ms += ms;
+    rbg::ensure_grid(ctx);
+    if (!ctx->have_pattern) {
+        RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+        rbg::setup_pattern(ctx);
+        RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+        RBG_CUDA(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->setup_ms += ms;
+    }
+    ctx->sys.reserve(ctx->sys_count());
 }
 
 void require_system(const rbg_ctx* ctx) {
@@ -207,13 +213,14 @@ rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_
         ctx->centres.reserve(m * dim);
         RBG_CUDA(cudaMemcpyAsync(ctx->centres.p, centres, m * dim * sizeof(double),
                                  cudaMemcpyHostToDevice, ctx->stream));
-        RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-        rbg::setup_centres(ctx);
-        RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
-        RBG_CUDA(cudaEventSynchronize(ctx->ev1));
-        float ms = 0.f;
-        RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
-        ctx->setup_ms = ms;
+        // everything derived from the centres is built at the first call that needs
+        // it (rbg::ensure_grid / require_pattern / the layout at the first assembly),
+        // so a host-array assembly can overlap it with the upload of the points
+        ctx->have_grid = false;
+        ctx->have_pattern = false;
+        ctx->bj_built = false;
+        ctx->lay = rbg::AsmLayout();
+        ctx->setup_ms = 0.0;
         ctx->have_centres = true;
     });
 }
@@ -250,7 +257,7 @@ rbg_status rbg_get_pattern(rbg_ctx* ctx, uint64_t* row_ptr, uint32_t* cols) {
 rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uint64_t n,
                         int accumulate, int validate) {
     return guarded(ctx, [&] {
-        require_pattern(ctx);
+        require_centres(ctx);
         if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
         bind(ctx);
         const int dim = ctx->dim;
@@ -272,7 +279,42 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
             ctx->in_h.reserve(n);
         }
         if (K == 1) {
-            if (n > 0) {
+            if (n > 0 && n * dim * sizeof(double) >= (size_t{64} << 20) && !rbg::page_locked(points)) {
+                // large pageable inputs: the staged upload (host copy threads + the copy
+                // engine, on the copy stream) overlaps the centre-side setup of this context
+                // -- tile grid, pattern and assembly layout, on the compute stream
+                if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+                if (!ctx->chunk_ev[0]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
+                RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->stream));  // earlier readers of in_pts / in_h
+                RBG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
+                std::exception_ptr up_err;
+                std::thread up([&] {
+                    try {
+                        RBG_CUDA(cudaSetDevice(ctx->device));
+                        rbg::h2d_on(ctx->copy_stream, ctx->in_pts.p, points, n * dim * sizeof(double));
+                        rbg::h2d_on(ctx->copy_stream, ctx->in_h.p, h, n * sizeof(double));
+                    } catch (...) {
+                        up_err = std::current_exception();
+                    }
+                });
+                try {
+                    require_pattern(ctx);
+                    if (!ctx->lay.built) rbg::build_layout(ctx, n);
+                } catch (...) {
+                    up.join();
+                    throw;
+                }
+                up.join();
+                if (up_err) std::rethrow_exception(up_err);
+                RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->copy_stream));
+                RBG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[0], 0));
+                if (validate) {
+                    const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, dim);
+                    if (bad < n)
+                        throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
+                }
+            } else if (n > 0) {
+                require_pattern(ctx);
                 rbg::h2d(ctx, ctx->in_pts.p, points, n * dim * sizeof(double));
                 rbg::h2d(ctx, ctx->in_h.p, h, n * sizeof(double));
                 if (validate) {  // kdtree.cpp:14-17, checked on the device copy (first offending index)
@@ -281,9 +323,11 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
                         throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
                 }
             }
+            require_pattern(ctx);  // (no-op when built above)
             rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
             return;
         }
+        require_pattern(ctx);
         if (!ctx->lay.built) rbg::build_layout(ctx, n);  // tile sizes follow the whole batch's density
         if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (int c = 0; c < K; ++c)
@@ -420,6 +464,7 @@ rbg_status rbg_evaluate_device(rbg_ctx* ctx, const double* d_c, const double* d_
     return guarded(ctx, [&] {
         require_centres(ctx);
         bind(ctx);
+        rbg::ensure_grid(ctx);
         rbg::evaluate_points(ctx, d_c, d_q, nq, d_f);
     });
 }
@@ -429,6 +474,7 @@ rbg_status rbg_evaluate(rbg_ctx* ctx, const double* c, const double* q, uint64_t
         require_centres(ctx);
         if (!c || (nq > 0 && (!q || !f))) throw Error(RBG_INVALID_ARGUMENT, "null array");
         bind(ctx);
+        rbg::ensure_grid(ctx);
         cudaStream_t st = ctx->stream;
         ctx->ev_c.reserve(ctx->m);
         RBG_CUDA(cudaMemcpyAsync(ctx->ev_c.p, c, ctx->m * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -450,6 +496,7 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
         if (n == 0) throw Error(RBG_INVALID_ARGUMENT, "error_report: empty cloud");  // model.cpp:198
         if (!c || !points || !h || !out) throw Error(RBG_INVALID_ARGUMENT, "null array");
         bind(ctx);
+        rbg::ensure_grid(ctx);
         cudaStream_t st = ctx->stream;
         ctx->ev_c.reserve(ctx->m);
         ctx->ev_q.reserve(n * ctx->dim);
@@ -471,11 +518,9 @@ rbg_status rbg_error_report(rbg_ctx* ctx, const double* c, const double* points,
 
 rbg_status rbg_set_poly(rbg_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
-        require_pattern(ctx);
-        bind(ctx);
+        require_centres(ctx);
+        if (ctx->poly_on != (enable != 0)) ctx->have_system = false;  // the system layout changes
         ctx->poly_on = enable != 0;
-        ctx->have_system = false;  // the system layout changes
-        ctx->sys.reserve(ctx->sys_count());
     });
 }
 

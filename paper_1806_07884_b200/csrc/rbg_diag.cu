@@ -114,6 +114,7 @@ extern "C" rbg_status rbg_support_counts(rbg_ctx* ctx, const double* q, uint64_t
     try {
         if (!ctx->have_centres) throw rbg::Error(RBG_NOT_READY, "no reference points set");
         RBG_CUDA(cudaSetDevice(ctx->device));
+        rbg::ensure_grid(ctx);
         cudaStream_t st = ctx->stream;
         ctx->ev_q.reserve(nq * ctx->dim + 1);
         // counters: allocated (8) by rbg_create

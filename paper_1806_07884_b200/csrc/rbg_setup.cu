@@ -306,6 +306,18 @@ void slot_maps(rbg_ctx* ctx, const uint64_t* cptr, uint64_t n_tiles, const uint3
     RBG_CHECK_LAUNCH(ctx);
 }
 
+void ensure_grid(rbg_ctx* ctx) {
+    if (ctx->have_grid) return;
+    RBG_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    setup_centres(ctx);
+    RBG_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    RBG_CUDA(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    RBG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->setup_ms += ms;
+    ctx->have_grid = true;
+}
+
 void setup_centres(rbg_ctx* ctx) {
     const int dim = ctx->dim;
     const uint64_t m = ctx->m;

@@ -357,8 +357,9 @@ bool page_locked(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-void h2d(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) {
-    cudaStream_t st = ctx->stream;
+void h2d(rbg_ctx* ctx, void* dst, const void* src, size_t bytes) { h2d_on(ctx->stream, dst, src, bytes); }
+
+void h2d_on(cudaStream_t st, void* dst, const void* src, size_t bytes) {
     if (bytes < kDirectBytes || page_locked(src)) {
         RBG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
         return;
