@@ -270,8 +270,9 @@ constexpr size_t kDirectBytes = size_t{16} << 20;
 class CopyPool {
   public:
     CopyPool() {
+        // leave a quarter of the cores to the caller: the centre-side setup overlaps the upload
         const unsigned hw = std::thread::hardware_concurrency();
-        nthreads_ = std::max(1u, std::min(16u, hw ? hw : 1u));
+        nthreads_ = std::max(1u, std::min(12u, hw ? (hw * 3) / 4 : 1u));
         for (unsigned t = 1; t < nthreads_; ++t) workers_.emplace_back([this, t] { run(t); });
     }
     ~CopyPool() {
