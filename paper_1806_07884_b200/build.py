@@ -29,7 +29,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      f"-I{ROOT / 'include'}"] + os.environ.get("RBG_NVCC_EXTRA", "").split()
 # the assembly kernels are split one translation unit per (dimension, family) so they compile in parallel
 CU_SOURCES = (["rbg_util.cu", "rbg_setup.cu", "rbg_layout.cu", "rbg_assemble.cu", "rbg_solve.cu",
-               "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu", "rbg_repass.cu"]
+               "rbg_eval.cu", "rbg_api.cu", "rbg_diag.cu", "rbg_repass.cu", "rbg_band.cu"]
               + [f"rbg_asm_part_{d}_{f}.cu" for d in (2, 3) for f in range(4)])
 
 LIB_RBG = PKG / "librbg.so"

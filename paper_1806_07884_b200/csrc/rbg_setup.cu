@@ -323,6 +323,7 @@ void setup_centres(rbg_ctx* ctx) {
     const uint64_t m = ctx->m;
     cudaStream_t st = ctx->stream;
     ctx->bj_built = false;  // preconditioner blocks follow the centre set
+    ctx->band = BandPlan();  // so does the banded-solve ordering
 
     // ---- bounding box (device reduction) + tile grid plan -------------------
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
