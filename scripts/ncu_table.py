@@ -23,10 +23,10 @@ for r in rows[2:]:
         except ValueError:
             return "-"
     t_unit = units[col["gpu__time_duration.sum"]]
-    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(t_unit, 1.0)
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(t_unit, 1.0)
     def mb(k):
         u = units[col[k]] if k in col else ""
-        sc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
+        sc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}.get(u, 1.0)
         return f(k, sc)
     st = [(h, r[i]) for h, i in col.items() if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")]
     tot = sum(float(v or 0) for _, v in st) or 1.0
