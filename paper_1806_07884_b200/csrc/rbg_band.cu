@@ -16,8 +16,8 @@
 //                   tile d >= 1 then solves L(J+d, J) = A(J+d, J) L_JJ^-T;
 //   band_update  -- one warp per trailing tile: A(J+d2, J+d1) -= L(J+d2, J)
 //                   L(J+d1, J)^T on the fp64 tensor cores (DMMA m8n8k4).
-// Forward / backward substitution: one kernel per tile row, each warp
-// re-solving the 32 x 32 diagonal block and applying one off-diagonal tile.
+// Forward / backward substitution: one CTA each, walking the tile rows (warp 0
+// solves the 32 x 32 diagonal block, the 32 warps apply the tiles below/above).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -157,12 +157,12 @@ __global__ void __launch_bounds__(32) band_panel_kernel(double* __restrict__ ban
     double x[TB];
 #pragma unroll
     for (int j = 0; j < TB; ++j) x[j] = ot[j * TB + lane];
+    // column-oriented: x_k /= L_kk, then x_j -= x_k L_jk for every j > k (independent updates)
 #pragma unroll
     for (int k = 0; k < TB; ++k) {
-        double s = x[k];
+        x[k] = x[k] / __shfl_sync(0xffffffffu, a[k], k);
 #pragma unroll
-        for (int q = 0; q < k; ++q) s = fma(-x[q], __shfl_sync(0xffffffffu, a[q], k), s);
-        x[k] = s / __shfl_sync(0xffffffffu, a[k], k);
+        for (int j = k + 1; j < TB; ++j) x[j] = fma(-x[k], __shfl_sync(0xffffffffu, a[k], j), x[j]);
     }
 #pragma unroll
     for (int j = 0; j < TB; ++j) ot[j * TB + lane] = x[j];
@@ -225,60 +225,75 @@ __global__ void __launch_bounds__(128) band_update_kernel(double* __restrict__ b
             }
 }
 
-// Forward substitution, tile row J: every warp solves L_JJ y_J = b_J (lane =
-// row) from the running right-hand side b (b_J is final once the kernels of
-// the earlier tile rows are done); warp d >= 1 applies b_{J+d} -= L(J+d, J) y_J,
-// warp 0 stores y_J (a separate vector: the other warps still read b_J).
-__global__ void __launch_bounds__(32) band_forward_kernel(const double* __restrict__ band, const double* __restrict__ diagL,
-                                                          uint64_t J, uint64_t nbb, double* __restrict__ b,
-                                                          double* __restrict__ yout) {
-    const int lane = threadIdx.x;
-    const uint64_t d = blockIdx.x;
-    const double* dt = diagL + J * (uint64_t)TE;
-    double y = b[J * TB + lane];
+// Forward substitution L y = b in one CTA (32 warps) over all tile rows: per
+// tile row J, warp 0 solves the 32 x 32 diagonal block (lane = row), then the
+// warps apply b_{J+d} -= L(J+d, J) y_J for the tiles below (d = warp + 32 i).
+constexpr int kSolveWarps = 32;
+__global__ void __launch_bounds__(kSolveWarps * 32) band_forward_kernel(const double* __restrict__ band,
+                                                                        const double* __restrict__ diagL,
+                                                                        uint64_t NT, uint64_t nbb,
+                                                                        double* __restrict__ b, double* __restrict__ y) {
+    __shared__ double yJ[TB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t J = 0; J < NT; ++J) {
+        if (warp == 0) {
+            const double* dt = diagL + J * (uint64_t)TE;
+            double v = b[J * TB + lane];
 #pragma unroll
-    for (int k = 0; k < TB; ++k) {
-        const double lk = dt[k * TB + lane];  // L(lane, k)
-        const double yk = __shfl_sync(0xffffffffu, y, k) / dt[k * TB + k];
-        if (lane == k) y = yk;
-        if (lane > k) y = fma(-lk, yk, y);
-    }
-    if (d == 0) {
-        yout[J * TB + lane] = y;
-        return;
-    }
-    const double* ot = band + (J * nbb + d) * (uint64_t)TE;  // L(J+d, J)
-    double s = 0.0;
+            for (int k = 0; k < TB; ++k) {
+                const double lk = dt[k * TB + lane];  // L(lane, k)
+                const double yk = __shfl_sync(0xffffffffu, v, k) / dt[k * TB + k];
+                if (lane == k) v = yk;
+                if (lane > k) v = fma(-lk, yk, v);
+            }
+            yJ[lane] = v;
+            y[J * TB + lane] = v;
+        }
+        __syncthreads();
+        const uint64_t dmax = min(nbb - 1, NT - 1 - J);
+        for (uint64_t d = 1 + warp; d <= dmax; d += kSolveWarps) {
+            const double* ot = band + (J * nbb + d) * (uint64_t)TE;  // L(J+d, J)
+            double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < TB; ++k) s = fma(ot[k * TB + lane], __shfl_sync(0xffffffffu, y, k), s);
-    b[(J + d) * TB + lane] -= s;
+            for (int k = 0; k < TB; ++k) s = fma(ot[k * TB + lane], yJ[k], s);
+            b[(J + d) * TB + lane] -= s;
+        }
+        __syncthreads();
+    }
 }
 
-// Backward substitution, tile row J (descending): every warp solves
-// L_JJ^T x_J = y_J from the running y; warp d >= 1 applies
-// y_{J-d} -= L(J, J-d)^T x_J, warp 0 stores x_J (separate vector).
-__global__ void __launch_bounds__(32) band_backward_kernel(const double* __restrict__ band, const double* __restrict__ diagL,
-                                                           uint64_t J, uint64_t nbb, double* __restrict__ y,
-                                                           double* __restrict__ xout) {
-    const int lane = threadIdx.x;
-    const uint64_t d = blockIdx.x;
-    const double* dt = diagL + J * (uint64_t)TE;
-    double x = y[J * TB + lane];
+// Backward substitution L^T x = y in one CTA, tile rows descending: warp 0
+// solves L_JJ^T x_J = y_J, the warps apply y_{J-d} -= L(J, J-d)^T x_J.
+__global__ void __launch_bounds__(kSolveWarps * 32) band_backward_kernel(const double* __restrict__ band,
+                                                                         const double* __restrict__ diagL,
+                                                                         uint64_t NT, uint64_t nbb,
+                                                                         double* __restrict__ y, double* __restrict__ x) {
+    __shared__ double xJ[TB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t J = NT; J-- > 0;) {
+        if (warp == 0) {
+            const double* dt = diagL + J * (uint64_t)TE;
+            double v = y[J * TB + lane];
 #pragma unroll
-    for (int k = TB - 1; k >= 0; --k) {
-        const double xk = __shfl_sync(0xffffffffu, x, k) / dt[k * TB + k];
-        if (lane == k) x = xk;
-        if (lane < k) x = fma(-dt[lane * TB + k], xk, x);  // L(k, lane)
-    }
-    if (d == 0) {
-        xout[J * TB + lane] = x;
-        return;
-    }
-    const double* ot = band + ((J - d) * nbb + d) * (uint64_t)TE;  // L(J, J-d): rows of J, columns of J-d
-    double s = 0.0;
+            for (int k = TB - 1; k >= 0; --k) {
+                const double xk = __shfl_sync(0xffffffffu, v, k) / dt[k * TB + k];
+                if (lane == k) v = xk;
+                if (lane < k) v = fma(-dt[lane * TB + k], xk, v);  // L(k, lane)
+            }
+            xJ[lane] = v;
+            x[J * TB + lane] = v;
+        }
+        __syncthreads();
+        const uint64_t dmax = min(nbb - 1, J);
+        for (uint64_t d = 1 + warp; d <= dmax; d += kSolveWarps) {
+            const double* ot = band + ((J - d) * nbb + d) * (uint64_t)TE;  // L(J, J-d): rows of J, columns of J-d
+            double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < TB; ++k) s = fma(ot[lane * TB + k], __shfl_sync(0xffffffffu, x, k), s);
-    y[(J - d) * TB + lane] -= s;
+            for (int k = 0; k < TB; ++k) s = fma(ot[lane * TB + k], xJ[k], s);
+            y[(J - d) * TB + lane] -= s;
+        }
+        __syncthreads();
+    }
 }
 
 template <bool TO_BAND>
@@ -423,16 +438,10 @@ void band_solve(rbg_ctx* ctx, double* c_out, rbg_solve_diag* diag) {
     }
     band_permute_kernel<true><<<blocks_for(padded, 256), 256, 0, st>>>(P.perm.p, m, padded, rhs, ctx->r.p);
     RBG_CHECK_LAUNCH(ctx);
-    for (uint64_t J = 0; J < NT; ++J) {  // L y = P rhs
-        band_forward_kernel<<<(unsigned)(std::min(nbb - 1, NT - 1 - J) + 1), 32, 0, st>>>(P.tiles.p, P.diag.p, J, nbb,
-                                                                                          ctx->r.p, ctx->z.p);
-        RBG_CHECK_LAUNCH(ctx);
-    }
-    for (uint64_t J = NT; J-- > 0;) {  // L^T x' = y
-        band_backward_kernel<<<(unsigned)(std::min(nbb - 1, J) + 1), 32, 0, st>>>(P.tiles.p, P.diag.p, J, nbb,
-                                                                                 ctx->z.p, ctx->q.p);
-        RBG_CHECK_LAUNCH(ctx);
-    }
+    band_forward_kernel<<<1, kSolveWarps * 32, 0, st>>>(P.tiles.p, P.diag.p, NT, nbb, ctx->r.p, ctx->z.p);  // L y = P rhs
+    RBG_CHECK_LAUNCH(ctx);
+    band_backward_kernel<<<1, kSolveWarps * 32, 0, st>>>(P.tiles.p, P.diag.p, NT, nbb, ctx->z.p, ctx->q.p);  // L^T x' = y
+    RBG_CHECK_LAUNCH(ctx);
     band_permute_kernel<false><<<blocks_for(padded, 256), 256, 0, st>>>(P.perm.p, m, padded, ctx->q.p, ctx->x.p);
     RBG_CHECK_LAUNCH(ctx);
     RBG_CUDA(cudaMemsetAsync(ctx->scal.p, 0, 2 * sizeof(double), st));
