@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) band_forward_kernel(const do
         if (warp == 0) {
             const double* dt = diagL + J * (uint64_t)TE;
             double v = b[J * TB + lane];
-#pragma unroll
+#pragma unroll 4
             for (int k = 0; k < TB; ++k) {
                 const double lk = dt[k * TB + lane];  // L(lane, k)
                 const double yk = __shfl_sync(0xffffffffu, v, k) / dt[k * TB + k];
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) band_forward_kernel(const do
         for (uint64_t d = 1 + warp; d <= dmax; d += kSolveWarps) {
             const double* ot = band + (J * nbb + d) * (uint64_t)TE;  // L(J+d, J)
             double s = 0.0;
-#pragma unroll
+#pragma unroll 8
             for (int k = 0; k < TB; ++k) s = fma(ot[k * TB + lane], yJ[k], s);
             b[(J + d) * TB + lane] -= s;
         }
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) band_backward_kernel(const d
         if (warp == 0) {
             const double* dt = diagL + J * (uint64_t)TE;
             double v = y[J * TB + lane];
-#pragma unroll
+#pragma unroll 4
             for (int k = TB - 1; k >= 0; --k) {
                 const double xk = __shfl_sync(0xffffffffu, v, k) / dt[k * TB + k];
                 if (lane == k) v = xk;
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kSolveWarps * 32) band_backward_kernel(const d
         for (uint64_t d = 1 + warp; d <= dmax; d += kSolveWarps) {
             const double* ot = band + ((J - d) * nbb + d) * (uint64_t)TE;  // L(J, J-d): rows of J, columns of J-d
             double s = 0.0;
-#pragma unroll
+#pragma unroll 8
             for (int k = 0; k < TB; ++k) s = fma(ot[lane * TB + k], xJ[k], s);
             y[(J - d) * TB + lane] -= s;
         }
