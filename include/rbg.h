@@ -112,16 +112,24 @@ rbg_status rbg_set_system(rbg_ctx* ctx, const double* values, const double* rhs,
                           const double* hits);
 
 /* ---- solve ------------------------------------------------------------------
- * Replaces solve_weights (solver.cpp:289-330).  Method: Jacobi-preconditioned
- * CG on the assembled SPD system, stopping when ||r||_2 <= tol*||b||_2
- * (tol <= 0 selects 1e-12) within max_iter (<= 0 selects 20000) iterations.
+ * Replaces solve_weights (solver.cpp:289-330).  Method: preconditioned CG on
+ * the assembled SPD system, stopping when ||r||_2 <= tol*||b||_2 (tol <= 0
+ * selects 1e-12) within max_iter (<= 0 selects 20000) iterations.  The
+ * preconditioner is a factorised sparse approximate inverse G^T G ~ B^-1 (one
+ * small dense Cholesky per centre over its pattern neighbours); point Jacobi
+ * for the bordered system or on request.  method RBG_SOLVE_BAND runs the
+ * reference's own factorisation instead: LLT of the x-ordered band.
  * Ridge ladder as the reference: lambda in {0,1e-10,1e-9,1e-8,1e-7,1e-6} x
- * trace/side added to the diagonal, next rung on breakdown, non-positive
- * diagonal or non-convergence; all rungs failing -> RBG_RUNTIME_ERROR with
+ * trace/side added to the diagonal, next rung on breakdown, a non-positive
+ * pivot or non-convergence; all rungs failing -> RBG_RUNTIME_ERROR with
  * the reference's message.  c_out: m doubles (host). */
+enum { RBG_SOLVE_AUTO = 0, RBG_SOLVE_PCG = 1, RBG_SOLVE_BAND = 2 };
+enum { RBG_PREC_AUTO = 0, RBG_PREC_FSAI = 1, RBG_PREC_JACOBI = 2 };
 typedef struct {
     double tol;
     int max_iter;
+    int method;  /* RBG_SOLVE_* (0 = automatic: PCG) */
+    int precond; /* RBG_PREC_*  (0 = automatic: FSAI, Jacobi with the border) */
 } rbg_solve_options;
 typedef struct {
     double ridge_lambda; /* SolveDiag::ridge_lambda */

@@ -66,7 +66,7 @@ class LayoutInfo(C.Structure):
 
 
 class SolveOptions(C.Structure):
-    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int)]
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("method", C.c_int), ("precond", C.c_int)]
 
 
 class SolveDiag(C.Structure):

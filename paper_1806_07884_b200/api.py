@@ -241,9 +241,13 @@ class Engine:
         self._check(self._L.rbg_set_system(self._ctx, _p(v), _p(r), _p(hh)))
 
     # --- solve / eval
-    def solve(self, tol: float = 0.0, max_iter: int = 0) -> tuple[np.ndarray, dict]:
+    def solve(self, tol: float = 0.0, max_iter: int = 0, method: str = "auto",
+              precond: str = "auto") -> tuple[np.ndarray, dict]:
+        """rbg_solve: method "auto" / "pcg" (FSAI-preconditioned CG) or "band" (the
+        reference's LLT on the x-ordered band); precond "auto" / "fsai" / "jacobi"."""
         c = np.empty(self.m)
-        opts = _native.SolveOptions(tol, max_iter)
+        opts = _native.SolveOptions(tol, max_iter, {"auto": 0, "pcg": 1, "band": 2}[method],
+                                    {"auto": 0, "fsai": 1, "jacobi": 2}[precond])
         diag = _native.SolveDiag()
         self._check(self._L.rbg_solve(self._ctx, C.byref(opts), _p(c), C.byref(diag)))
         return c, {k: getattr(diag, k) for k, _ in diag._fields_}

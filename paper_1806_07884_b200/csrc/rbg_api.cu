@@ -219,6 +219,7 @@ rbg_status rbg_set_centres(rbg_ctx* ctx, int dim, const double* centres, uint64_
         ctx->have_grid = false;
         ctx->have_pattern = false;
         ctx->bj_built = false;
+        ctx->fs_built = false;
         ctx->lay = rbg::AsmLayout();
         ctx->setup_ms = 0.0;
         ctx->have_centres = true;

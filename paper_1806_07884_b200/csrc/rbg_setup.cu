@@ -322,7 +322,8 @@ void setup_centres(rbg_ctx* ctx) {
     const int dim = ctx->dim;
     const uint64_t m = ctx->m;
     cudaStream_t st = ctx->stream;
-    ctx->bj_built = false;  // preconditioner blocks follow the centre set
+    ctx->bj_built = false;  // solve order and preconditioner pattern follow the centre set
+    ctx->fs_built = false;
     ctx->band = BandPlan();  // so does the banded-solve ordering
 
     // ---- bounding box (device reduction) + tile grid plan -------------------

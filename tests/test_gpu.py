@@ -397,15 +397,14 @@ print("c", np.max(np.abs(c - oc)) / np.max(np.abs(oc)), d["iterations"])
 """
 
 
-@pytest.mark.parametrize("env", [{"RBG_H2D_CHUNKS": "3"}, {"RBG_PREC": "jacobi", "RBG_SOLVER": "pcg"},
-                                 {"RBG_PERM_UNSORTED": "1", "RBG_SOLVER": "pcg"}, {"RBG_SOLVER": "pcg"},
+@pytest.mark.parametrize("env", [{"RBG_H2D_CHUNKS": "3"}, {"RBG_PREC": "jacobi"}, {"RBG_FSAI_RHO": "1.0"},
                                  {"RBG_SOLVER": "band"}])
 def test_chunked_upload_and_point_jacobi_paths(env):
-    """The chunked pinned-upload path of rbg_assemble (accumulating chunks), both
-    solvers (the banded LLT, default at cfg2, and the block-Jacobi PCG), the
-    point-Jacobi PCG (RBG_PREC=jacobi) and the Morton-order solve CSR without
-    the in-row column sort, against the oracle, cfg2 geometry at 1.2e6 points
-    (the knobs are read once per process or centre set, hence a subprocess)."""
+    """The chunked pinned-upload path of rbg_assemble (accumulating chunks), the
+    point-Jacobi PCG (RBG_PREC=jacobi), the FSAI PCG with a distance-restricted
+    pattern and the banded LLT forced from the environment, against the oracle,
+    cfg2 geometry at 1.2e6 points (the knobs are read once per process or centre
+    set, hence a subprocess)."""
     import os
     import subprocess
     import sys
