@@ -61,14 +61,6 @@ struct BorderDev {
 constexpr int kThreads = 256;
 constexpr int kBatch = 32;
 constexpr int kBatchFsai = 8;
-// FSAI pattern radius in support radii (RBG_FSAI_RHO overrides): the pattern of B is rho = 2
-#ifndef RBG_FSAI_RHO2
-#define RBG_FSAI_RHO2 1.25
-#endif
-#ifndef RBG_FSAI_RHO3
-#define RBG_FSAI_RHO3 1.0
-#endif
-constexpr double kFsaiRho2 = RBG_FSAI_RHO2, kFsaiRho3 = RBG_FSAI_RHO3;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -367,6 +359,27 @@ __global__ void bj_pos_kernel(const uint32_t* __restrict__ perm, uint64_t m, uin
         pos[perm[k]] = (uint32_t)k;
 }
 
+// Sweep order of the FSAI factor: rank of every Morton position when the
+// centres are sorted by (x, y, z).  "Lower" in that order is a half-space, so
+// every row of G sees about half of its neighbourhood (in Morton order the
+// share swings between none and all of it along the curve).
+__global__ void rank_keys_kernel(const double* __restrict__ centres, const uint32_t* __restrict__ perm, uint64_t m,
+                                 int dim, double lo0, double lo1, double lo2, double scale,
+                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = perm[k];
+        const double lo[3] = {lo0, lo1, lo2};
+        const double qmax = dim == 2 ? 4294967295.0 : 2097151.0;
+        uint64_t key = 0;
+        for (int d = 0; d < dim; ++d) {
+            const double q = fmin(fmax((centres[i * dim + d] - lo[d]) * scale * qmax, 0.0), qmax);
+            key = (key << (dim == 2 ? 32 : 21)) | (uint64_t)q;
+        }
+        keys[k] = key;
+        ids[k] = (uint32_t)k;
+    }
+}
+
 // Full CSR in Morton order: new row k = centre perm[k], columns renumbered by
 // pos and sorted ascending within the row (segmented sort), then pf2u = the
 // upper-CSR slot of every entry (binary search in the ascending upper rows).
@@ -458,6 +471,20 @@ void build_solve_order(rbg_ctx* ctx) {
                                              64, st));
     bj_pos_kernel<<<blocks_for(m, 256), 256, 0, st>>>(ctx->bj_perm.p, m, ctx->bj_pos.p);
     RBG_CHECK_LAUNCH(ctx);
+    {  // sweep rank of every Morton position (stable sort: ties keep their Morton order)
+        DevBuf<uint32_t> order;
+        order.reserve(m);
+        ctx->prank.reserve(m);
+        rank_keys_kernel<<<blocks_for(m, 256), 256, 0, st>>>(ctx->centres.p, ctx->bj_perm.p, m, ctx->dim,
+                                                            ctx->grid.lo[0], ctx->grid.lo[1], ctx->grid.lo[2],
+                                                            span > 0.0 ? 1.0 / span : 1.0, keys.p, ids.p);
+        RBG_CHECK_LAUNCH(ctx);
+        RBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys_out.p, ids.p, order.p, (int)m, 0, 64,
+                                                 st));
+        bj_pos_kernel<<<blocks_for(m, 256), 256, 0, st>>>(order.p, m, ctx->prank.p);
+        RBG_CHECK_LAUNCH(ctx);
+        RBG_CUDA(cudaStreamSynchronize(st));
+    }
     DevBuf<uint32_t> len;
     len.reserve(m + 1);
     ctx->pfptr.reserve(m + 1);
@@ -482,72 +509,133 @@ void build_solve_order(rbg_ctx* ctx) {
 
 // ------------------------------------------------------ FSAI preconditioner
 // Factorised sparse approximate inverse (Kolotilina-Yeremin): G ~ L^-1 for
-// B + shift I = L L^T, lower triangular in the solve order with the prescribed
-// pattern  P_k = { j <= k : (k, j) in the pattern of B, |c_k - c_j| < rho r }.
-// Row k of G is the last row of chol(B[P_k, P_k])^-1 -- one small dense SPD
-// factorisation per centre, all independent -- and M^-1 = G^T G.  A^T A of
-// compactly supported kernels is ill-conditioned through its local oscillatory
-// modes, which these local factorisations capture: the CG iteration count
-// drops from O(1000) (block Jacobi) to O(10) at rho = 2 for one extra
-// SpMV-sized sweep per iteration (G and G^T together have the nonzeros of B
-// at rho = 2).  A non-positive local pivot fails the attempt, so the
-// reference's ridge ladder (solver.cpp:296-315) moves to the next lambda.
-constexpr int kFsaiCap = 128;    // longest row of G the setup kernel factors (rho shrinks until it fits)
-constexpr int kFsaiMaxT = kFsaiCap / 32;
+// B + shift I = L L^T in the sweep order (centres sorted by x, y, z) with the
+// prescribed pattern  P_k = the (up to) 31 nearest pattern neighbours of k that
+// come before it in the sweep (within rho r) + {k}.  Row k of G is the last row
+// of chol(B[P_k, P_k])^-1 with k ordered last -- one 32 x 32 dense SPD
+// factorisation per centre, all independent, held in the registers of one
+// warp -- and M^-1 = G^T G.  A^T A of compactly supported kernels is
+// ill-conditioned through its local oscillatory modes, which these local
+// factorisations capture: the CG iteration count drops from O(1000) (block
+// Jacobi) to ~40.  (The whole pattern of B as P_k gives 13-17 iterations, but
+// its 81 x 81 factorisations cost more than the iterations they save.)  G and
+// G^T are stored as two CSRs with Morton-ordered rows (the order the CG
+// vectors live in); nothing needs G to be triangular in that order.  A
+// non-positive local pivot fails the attempt, so the reference's ridge ladder
+// (solver.cpp:296-315) moves to the next lambda.
+constexpr int kFsaiN = 32;       // rows of a local system: one per lane
+constexpr int kFsaiWarps = 4;    // warps per CTA in the pattern and setup kernels
 
-__device__ __forceinline__ bool fsai_keep(const double* __restrict__ centres, int dim, uint32_t ci, uint32_t cj,
-                                          double rad2) {
-    if (ci == cj || rad2 < 0.0) return true;
+__device__ __forceinline__ double fsai_dist2(const double* __restrict__ centres, int dim, uint32_t ci, uint32_t cj) {
     double d2 = 0.0;
     for (int d = 0; d < dim; ++d) {
         const double t = centres[(uint64_t)ci * dim + d] - centres[(uint64_t)cj * dim + d];
         d2 += t * t;
     }
-    return d2 < rad2;
+    return d2;
 }
 
-// FILL = false: row lengths of G (cols <= k) and G^T (cols >= k) and the longest
-// G row; FILL = true: the column lists (ascending, order-preserving compaction).
+// tau[k]: squared radius below which row k keeps its earlier-in-sweep
+// neighbours -- the largest of 24 bisection steps in (0, rad2] that keeps at
+// most kFsaiN - 1 of them; glen[k] = that count + 1 (k itself).
+__global__ void __launch_bounds__(kFsaiWarps * 32) fsai_radius_kernel(
+    const uint64_t* __restrict__ pfptr, const uint32_t* __restrict__ pfcols, const uint32_t* __restrict__ perm,
+    const uint32_t* __restrict__ rank, const double* __restrict__ centres, int dim, double rad2, uint64_t m,
+    uint32_t rowcap, double* __restrict__ tau, uint32_t* __restrict__ glen) {
+    extern __shared__ double fr_sm[];  // per warp: squared distances of the earlier neighbours
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* dd = fr_sm + (size_t)w * rowcap;
+    const uint64_t warps = (uint64_t)gridDim.x * kFsaiWarps;
+    for (uint64_t k = blockIdx.x * (uint64_t)kFsaiWarps + w; k < m; k += warps) {
+        const uint32_t ci = perm[k], rk = rank[k];
+        const uint64_t e0 = pfptr[k];
+        const int len = (int)(pfptr[k + 1] - e0);
+        for (int e = lane; e < len; e += 32) {
+            const uint32_t c = pfcols[e0 + e];
+            dd[e] = (c != (uint32_t)k && rank[c] < rk) ? fsai_dist2(centres, dim, ci, perm[c]) : 1e300;
+        }
+        __syncwarp();
+        const auto count_below = [&](double t) {
+            int n = 0;
+            for (int e = lane; e < len; e += 32) n += dd[e] < t ? 1 : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+            return n;
+        };
+        double hi = rad2;
+        int n = count_below(hi);
+        if (n > kFsaiN - 1) {
+            double lo = 0.0;  // count_below(lo) = 0
+            n = 0;
+            for (int it = 0; it < 24; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                const int nm = count_below(mid);
+                if (nm > kFsaiN - 1) {
+                    hi = mid;
+                } else {
+                    lo = mid;
+                    n = nm;
+                }
+            }
+            hi = lo;
+        }
+        if (lane == 0) {
+            tau[k] = hi;
+            glen[k] = (uint32_t)n + 1u;
+        }
+        __syncwarp();
+    }
+}
+
+// FILL = false: row lengths of G^T (row j: every k after j in the sweep that
+// keeps j, and j itself); FILL = true: the column lists of G and G^T, ascending
+// in Morton position (order-preserving compaction), k itself last in its G row.
 template <bool FILL>
 __global__ void fsai_pattern_kernel(const uint64_t* __restrict__ pfptr, const uint32_t* __restrict__ pfcols,
-                                    const uint32_t* __restrict__ perm, const double* __restrict__ centres, int dim,
-                                    double rad2, uint64_t m, uint32_t* __restrict__ glen, uint32_t* __restrict__ tlen,
-                                    unsigned* __restrict__ gmax, const uint64_t* __restrict__ gptr,
+                                    const uint32_t* __restrict__ perm, const uint32_t* __restrict__ rank,
+                                    const double* __restrict__ centres, int dim, const double* __restrict__ tau,
+                                    uint64_t m, uint32_t* __restrict__ tlen, const uint64_t* __restrict__ gptr,
                                     const uint64_t* __restrict__ tptr, uint32_t* __restrict__ gcols,
                                     uint32_t* __restrict__ tcols) {
     const int lane = threadIdx.x & 31;
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
     for (uint64_t k = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5); k < m; k += warps) {
-        const uint32_t ci = perm[k];
+        const uint32_t ci = perm[k], rk = rank[k];
+        const double tk = tau[k];
         const uint64_t e0 = pfptr[k], e1 = pfptr[k + 1];
         uint32_t nl = 0, nu = 0;
         for (uint64_t eb = e0; eb < e1; eb += 32) {
             const uint64_t e = eb + lane;
             uint32_t c = 0;
-            bool keep = false;
+            bool lower = false, upper = false;
             if (e < e1) {
                 c = pfcols[e];
-                keep = fsai_keep(centres, dim, ci, perm[c], rad2);
+                if (c == (uint32_t)k) {
+                    upper = true;  // the diagonal: in G^T's row here, appended to G's row below
+                } else {
+                    const double d2 = fsai_dist2(centres, dim, ci, perm[c]);
+                    if (rank[c] < rk) lower = FILL && d2 < tk;
+                    else upper = d2 < tau[c];
+                }
             }
-            const unsigned lo = __ballot_sync(0xffffffffu, keep && c <= (uint32_t)k);
-            const unsigned up = __ballot_sync(0xffffffffu, keep && c >= (uint32_t)k);
+            const unsigned lo = __ballot_sync(0xffffffffu, lower);
+            const unsigned up = __ballot_sync(0xffffffffu, upper);
             if (FILL) {
                 const unsigned below = (1u << lane) - 1u;
-                if (keep && c <= (uint32_t)k) gcols[gptr[k] + nl + __popc(lo & below)] = c;
-                if (keep && c >= (uint32_t)k) tcols[tptr[k] + nu + __popc(up & below)] = c;
+                if (lower) gcols[gptr[k] + nl + __popc(lo & below)] = c;
+                if (upper) tcols[tptr[k] + nu + __popc(up & below)] = c;
             }
             nl += __popc(lo);
             nu += __popc(up);
         }
-        if (!FILL && lane == 0) {
-            glen[k] = nl;
-            tlen[k] = nu;
-            atomicMax(gmax, nl);
+        if (lane == 0) {
+            if (FILL) gcols[gptr[k] + nl] = (uint32_t)k;
+            else tlen[k] = nu;
         }
     }
 }
 
-// tmap[e] for the G^T entry (row j, column k >= j): where G's entry (k, j) lives.
+// tmap[e] for the G^T entry (row j, column k): where G's entry (k, j) lives.
 __global__ void fsai_tmap_kernel(const uint64_t* __restrict__ tptr, const uint32_t* __restrict__ tcols,
                                  const uint64_t* __restrict__ gptr, const uint32_t* __restrict__ gcols, uint64_t m,
                                  uint32_t* __restrict__ tmap) {
@@ -556,7 +644,8 @@ __global__ void fsai_tmap_kernel(const uint64_t* __restrict__ tptr, const uint32
     for (uint64_t j = blockIdx.x * (uint64_t)(blockDim.x / 32) + (threadIdx.x >> 5); j < m; j += warps) {
         for (uint64_t e = tptr[j] + lane; e < tptr[j + 1]; e += 32) {
             const uint32_t k = tcols[e];
-            uint64_t lo = gptr[k], hi = gptr[k + 1];
+            uint64_t lo = gptr[k], hi = gptr[k + 1] - 1;  // the last entry of G's row k is k itself
+            if (k == (uint32_t)j) lo = hi;
             while (lo < hi) {
                 const uint64_t mid = (lo + hi) >> 1;
                 if (gcols[mid] < (uint32_t)j) lo = mid + 1; else hi = mid;
@@ -573,125 +662,96 @@ __global__ void fsai_transpose_kernel(const uint32_t* __restrict__ tmap, const d
         tvals[e] = gvals[tmap[e]];
 }
 
-// Shared-memory region of one warp of the setup kernel (bytes): packed lower
-// triangle S (column-major, + one 32-row slab of slack for the unpredicated
-// loads of the factorisation), x, 1 / diag, the pattern P and a row buffer.
-__host__ __device__ inline uint32_t fsai_region(uint32_t nmax, uint32_t rowcap) {
-    const uint32_t tri = nmax * (nmax + 1) / 2 + 32;
-    return (tri * 8u + nmax * 8u * 2u + nmax * 4u + rowcap * 4u + 15u) & ~15u;
+// One warp per row k of G; lane a owns local row a (P[a], k last).
+//  gather     for every a, lane b <= a finds P[b] in B's row P[a] (columns
+//             ascending: binary search) and files B[P[a], P[b]] into S[a][b]
+//             in shared memory, from where lane a takes its row;
+//  factorise  right-looking Cholesky of the 32 x 32 system with row a in the
+//             registers of lane a: per column one pivot broadcast and one
+//             shuffle + FMA per trailing column (rows past n are identity);
+//  solve      x^T L = e_n^T from the last row up: x = row k of G.
+constexpr int kFsaiStages = 4;  // row buffers in flight per warp (cp.async)
+inline size_t fsai_setup_smem(uint32_t rowcap) {
+    return (size_t)kFsaiWarps * (kFsaiN * (kFsaiN + 1) * sizeof(double) + (size_t)kFsaiStages * rowcap * sizeof(uint32_t));
 }
 
-// One warp per row k of G.
-//  gather     S = (B + shift I)[P, P], lower triangle: for every a, the lower
-//             part of B's (sorted) row P[a] is staged and searched for P[b], b <= a;
-//  factorise  left-looking Cholesky, lanes over the rows of a column, the
-//             column-to-the-left loop unrolled over four independent sums;
-//  solve      L^T x = e_n column by column: x = last row of L^-1 = row k of G.
-template <int MAXT>
-__global__ void __launch_bounds__(128) fsai_setup_kernel(const uint64_t* __restrict__ pfptr,
-                                                         const uint32_t* __restrict__ pfcols,
-                                                         const double* __restrict__ vfull,
-                                                         const uint64_t* __restrict__ gptr,
-                                                         const uint32_t* __restrict__ gcols, uint64_t m, uint32_t nmax,
-                                                         uint32_t rowcap, const uint32_t* __restrict__ perm,
-                                                         double* scal, double* __restrict__ gvals) {
+__global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
+    const uint64_t* __restrict__ pfptr, const uint32_t* __restrict__ pfcols, const double* __restrict__ vfull,
+    const uint64_t* __restrict__ gptr, const uint32_t* __restrict__ gcols, uint64_t m, uint32_t rowcap,
+    const uint32_t* __restrict__ perm, double* scal, double* __restrict__ gvals) {
     if (scal[S_FAIL] != 0.0) return;
     extern __shared__ __align__(16) unsigned char fs_sm[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    unsigned char* base = fs_sm + (size_t)w * fsai_region(nmax, rowcap);
-    double* S = reinterpret_cast<double*>(base);
-    double* x = S + (nmax * (nmax + 1) / 2 + 32);
-    double* dinv = x + nmax;
-    uint32_t* P = reinterpret_cast<uint32_t*>(dinv + nmax);
-    uint32_t* rowbuf = P + nmax;
+    double (*S)[kFsaiN + 1] = reinterpret_cast<double (*)[kFsaiN + 1]>(fs_sm) + (size_t)w * kFsaiN;
+    uint32_t* rbuf = reinterpret_cast<uint32_t*>(fs_sm + (size_t)kFsaiWarps * kFsaiN * (kFsaiN + 1) * sizeof(double)) +
+                     (size_t)w * kFsaiStages * rowcap;
     const double shift = scal[S_SHIFT];
-    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
-    for (uint64_t k = blockIdx.x * (uint64_t)(blockDim.x / 32) + w; k < m; k += warps) {
+    const uint64_t warps = (uint64_t)gridDim.x * kFsaiWarps;
+    for (uint64_t k = blockIdx.x * (uint64_t)kFsaiWarps + w; k < m; k += warps) {
         const uint64_t g0 = gptr[k];
         const int n = (int)(gptr[k + 1] - g0);
-        const int ntri = n * (n + 1) / 2;
-        for (int a = lane; a < n; a += 32) P[a] = gcols[g0 + a];
-        for (int t = lane; t < ntri; t += 32) S[t] = 0.0;
-        __syncwarp();
-        // ---- gather (element (i, j), i >= j, at j n - j (j - 1) / 2 - j + i)
+        const uint32_t mine = lane < n ? gcols[g0 + lane] : 0u;
+        const uint64_t my0 = pfptr[mine];
+        const uint32_t mylen = (uint32_t)(pfptr[mine + 1] - my0);
+        // the columns of B's row P[a] -> row buffer a % kFsaiStages (asynchronous)
+        const auto issue_row = [&](int a) {
+            if (a < n) {
+                const uint64_t e0 = __shfl_sync(0xffffffffu, my0, a);
+                const uint32_t len = __shfl_sync(0xffffffffu, mylen, a);
+                uint32_t* dst = rbuf + (a % kFsaiStages) * rowcap;
+                for (uint32_t e = lane; e < len; e += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(dst + e)),
+                                 "l"(pfcols + e0 + e)
+                                 : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+#pragma unroll
+        for (int a = 0; a < kFsaiStages - 1; ++a) issue_row(a);
+#pragma unroll
+        for (int j = 0; j < kFsaiN; ++j) S[lane][j] = j == lane && lane >= n ? 1.0 : 0.0;
+        // S[a][b] = B[P[a], P[b]] for b <= a: lane b looks P[b] up in B's row P[a]
+        // (columns ascending: a branch-free lower bound in the staged row); the
+        // value load of one row is consumed while the next row is searched
+        double vprev = 0.0;
+        bool hprev = false;
         for (int a = 0; a < n; ++a) {
-            const uint32_t ra = P[a];
-            const uint64_t e0 = pfptr[ra];
-            // lower part of row ra = the entries up to its diagonal (columns ascending)
-            int nlow = 0;
-            for (uint64_t eb = e0; eb < pfptr[ra + 1]; eb += 32) {
-                const uint64_t e = eb + lane;
-                const uint32_t c = e < pfptr[ra + 1] ? pfcols[e] : 0xffffffffu;
-                const bool low = c <= ra;
-                if (low) rowbuf[(int)(eb - e0) + lane] = c;
-                const unsigned bl = __ballot_sync(0xffffffffu, low);
-                nlow += __popc(bl);
-                if (bl != 0xffffffffu) break;
-            }
+            issue_row(a + kFsaiStages - 1);
+            asm volatile("cp.async.wait_group %0;" ::"n"(kFsaiStages - 1) : "memory");
             __syncwarp();
-            for (int b = lane; b <= a; b += 32) {
-                const uint32_t want = P[b];
-                int lo = 0, hi = nlow;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (rowbuf[mid] < want) lo = mid + 1; else hi = mid;
-                }
-                if (lo < nlow && rowbuf[lo] == want) {
-                    const double v = vfull[e0 + lo];
-                    S[b * n - ((b * (b - 1)) >> 1) - b + a] = b == a ? v + shift : v;
-                }
-            }
-            __syncwarp();
+            const uint64_t e0 = __shfl_sync(0xffffffffu, my0, a);
+            const uint32_t len = __shfl_sync(0xffffffffu, mylen, a);
+            const uint32_t* rc = rbuf + (a % kFsaiStages) * rowcap;
+            uint32_t lo = 0;
+            for (uint32_t step = 1u << (31 - __clz(len)); step > 0; step >>= 1)
+                if (lo + step <= len && rc[lo + step - 1] < mine) lo += step;
+            const bool hit = lane <= a && lo < len && rc[lo] == mine;
+            const double v = hit ? vfull[e0 + lo] : 0.0;
+            if (hprev) S[a - 1][lane] = lane == a - 1 ? vprev + shift : vprev;
+            vprev = v;
+            hprev = hit;
+            __syncwarp();  // the buffer is refilled kFsaiStages - 1 rows from now
         }
-        // ---- left-looking Cholesky
+        if (hprev) S[n - 1][lane] = lane == n - 1 ? vprev + shift : vprev;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        double row[kFsaiN];
+#pragma unroll
+        for (int j = 0; j < kFsaiN; ++j) row[j] = S[lane][j];
         bool bad = false;
-        for (int c = 0; c < n; ++c) {
-            const int Tc = (n - c + 31) >> 5;  // 32-row slabs of this column (warp-uniform)
-            const int offc = c * n - ((c * (c - 1)) >> 1) - c;
-            double a0[MAXT], a1[MAXT], a2[MAXT], a3[MAXT];
 #pragma unroll
-            for (int t = 0; t < MAXT; ++t) {
-                a0[t] = t < Tc ? S[offc + c + lane + 32 * t] : 0.0;
-                a1[t] = a2[t] = a3[t] = 0.0;
-            }
-            int j = 0, oj = 0;
-            for (; j + 4 <= c; j += 4) {
-                const int o0 = oj, o1 = o0 + (n - j - 1), o2 = o1 + (n - j - 2), o3 = o2 + (n - j - 3);
-                const double l0 = S[o0 + c], l1 = S[o1 + c], l2 = S[o2 + c], l3 = S[o3 + c];
-#pragma unroll
-                for (int t = 0; t < MAXT; ++t)
-                    if (t < Tc) {
-                        const int i = c + lane + 32 * t;
-                        a0[t] = fma(-S[o0 + i], l0, a0[t]);
-                        a1[t] = fma(-S[o1 + i], l1, a1[t]);
-                        a2[t] = fma(-S[o2 + i], l2, a2[t]);
-                        a3[t] = fma(-S[o3 + i], l3, a3[t]);
-                    }
-                oj = o3 + (n - j - 4);
-            }
-            for (; j < c; ++j) {
-                const double l0 = S[oj + c];
-#pragma unroll
-                for (int t = 0; t < MAXT; ++t)
-                    if (t < Tc) a0[t] = fma(-S[oj + c + lane + 32 * t], l0, a0[t]);
-                oj += n - j - 1;
-            }
-#pragma unroll
-            for (int t = 0; t < MAXT; ++t) a0[t] = (a0[t] + a1[t]) + (a2[t] + a3[t]);
-            double d = __shfl_sync(0xffffffffu, a0[0], 0);  // row c is lane 0 of slab 0
+        for (int j = 0; j < kFsaiN; ++j) {
+            double d = __shfl_sync(0xffffffffu, row[j], j);
             if (!(d > 0.0) || !isfinite(d)) {
                 bad = true;
                 d = 1.0;
             }
-            const double s = sqrt(d), inv = 1.0 / s;
-            __syncwarp();
+            const double inv = rsqrt(d);
+            const double lj = row[j] * inv;  // column j of L (rows >= j; lane j: sqrt(d))
+            row[j] = lj;
 #pragma unroll
-            for (int t = 0; t < MAXT; ++t) {
-                const int i = c + lane + 32 * t;
-                if (t < Tc && i < n) S[offc + i] = i == c ? s : a0[t] * inv;
-            }
-            if (lane == 0) dinv[c] = inv;
-            __syncwarp();
+            for (int c = j + 1; c < kFsaiN; ++c) row[c] = fma(-lj, __shfl_sync(0xffffffffu, lj, c), row[c]);
         }
         if (bad) {
             if (lane == 0) {
@@ -701,17 +761,16 @@ __global__ void __launch_bounds__(128) fsai_setup_kernel(const uint64_t* __restr
             }
             continue;
         }
-        // ---- L^T x = e_n, column oriented (row i of L updates x[0..i))
-        for (int a = lane; a < n; a += 32) x[a] = a == n - 1 ? 1.0 : 0.0;
-        __syncwarp();
-        for (int i = n - 1; i >= 0; --i) {
-            const double xi = x[i] * dinv[i];
-            __syncwarp();
-            if (lane == 0) x[i] = xi;
-            for (int j2 = lane; j2 < i; j2 += 32) x[j2] = fma(-S[j2 * n - ((j2 * (j2 - 1)) >> 1) - j2 + i], xi, x[j2]);
-            __syncwarp();
+        // x_i = ([i == n - 1] - sum_{i' > i} x_i' L[i'][i]) / L[i][i]
+        double x = 0.0;
+#pragma unroll
+        for (int i = kFsaiN - 1; i >= 0; --i) {
+            double t = lane > i ? x * row[i] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == i) x = ((i == n - 1 ? 1.0 : 0.0) - t) / row[i];
         }
-        for (int a = lane; a < n; a += 32) gvals[g0 + a] = x[a];
+        if (lane < n) gvals[g0 + lane] = x;
         __syncwarp();
     }
 }
@@ -812,27 +871,23 @@ void fsai_build(rbg_ctx* ctx) {
         const char* e = std::getenv("RBG_FSAI_RHO");
         return e ? std::atof(e) : 0.0;
     }();
-    double rho = rho_env > 0.0 ? rho_env : (ctx->dim == 2 ? kFsaiRho2 : kFsaiRho3);
+    const double rho = rho_env > 0.0 ? std::min(rho_env, 2.0) : 2.0;  // 2 = anywhere in the pattern of B
+    const double rad2 = rho >= 2.0 ? 8.0 * ctx->r2 : rho * rho * ctx->r2;
     DevBuf<uint32_t> glen, tlen;
-    DevBuf<unsigned> gmax;
+    DevBuf<double> tau;
     glen.reserve(m + 1);
     tlen.reserve(m + 1);
-    gmax.reserve(1);
-    const unsigned gw = blocks_for(m, 8, 148u * 16u);
-    unsigned nmax = 0;
-    double rad2 = -1.0;
-    for (;;) {
-        rad2 = rho >= 2.0 ? -1.0 : rho * rho * ctx->r2;
-        RBG_CUDA(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned), st));
-        fsai_pattern_kernel<false><<<gw, 256, 0, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->bj_perm.p, ctx->centres.p,
-                                                        ctx->dim, rad2, m, glen.p, tlen.p, gmax.p, nullptr, nullptr,
-                                                        nullptr, nullptr);
-        RBG_CHECK_LAUNCH(ctx);
-        RBG_CUDA(cudaMemcpyAsync(&nmax, gmax.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        RBG_CUDA(cudaStreamSynchronize(st));
-        if (nmax <= (unsigned)kFsaiCap) break;
-        rho = std::min(rho, 2.0) * 0.85;  // clustered centres: shrink the pattern until every row fits
-    }
+    tau.reserve(m);
+    const unsigned gw = blocks_for(m, kFsaiWarps, 148u * 16u);
+    const uint32_t rowcap = (ctx->max_full_row + 31u) & ~31u;
+    fsai_radius_kernel<<<gw, kFsaiWarps * 32, (size_t)kFsaiWarps * rowcap * sizeof(double), st>>>(
+        ctx->pfptr.p, ctx->pfcols.p, ctx->bj_perm.p, ctx->prank.p, ctx->centres.p, ctx->dim, rad2, m, rowcap, tau.p,
+        glen.p);
+    RBG_CHECK_LAUNCH(ctx);
+    fsai_pattern_kernel<false><<<gw, kFsaiWarps * 32, 0, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->bj_perm.p,
+                                                                ctx->prank.p, ctx->centres.p, ctx->dim, tau.p, m, tlen.p,
+                                                                nullptr, nullptr, nullptr, nullptr);
+    RBG_CHECK_LAUNCH(ctx);
     ctx->fs_gptr.reserve(m + 1);
     ctx->fs_tptr.reserve(m + 1);
     exclusive_scan_u32_to_u64(ctx, glen.p, ctx->fs_gptr.p, m);
@@ -847,63 +902,30 @@ void fsai_build(rbg_ctx* ctx) {
     ctx->fs_gvals.reserve(nnz);
     ctx->fs_tvals.reserve(nnz);
     ctx->fs_u.reserve(m);
-    fsai_pattern_kernel<true><<<gw, 256, 0, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->bj_perm.p, ctx->centres.p, ctx->dim,
-                                                   rad2, m, nullptr, nullptr, nullptr, ctx->fs_gptr.p, ctx->fs_tptr.p,
-                                                   ctx->fs_gcols.p, ctx->fs_tcols.p);
+    fsai_pattern_kernel<true><<<gw, kFsaiWarps * 32, 0, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->bj_perm.p, ctx->prank.p,
+                                                               ctx->centres.p, ctx->dim, tau.p, m, nullptr,
+                                                               ctx->fs_gptr.p, ctx->fs_tptr.p, ctx->fs_gcols.p,
+                                                               ctx->fs_tcols.p);
     RBG_CHECK_LAUNCH(ctx);
-    fsai_tmap_kernel<<<gw, 256, 0, st>>>(ctx->fs_tptr.p, ctx->fs_tcols.p, ctx->fs_gptr.p, ctx->fs_gcols.p, m,
-                                         ctx->fs_tmap.p);
+    fsai_tmap_kernel<<<gw, kFsaiWarps * 32, 0, st>>>(ctx->fs_tptr.p, ctx->fs_tcols.p, ctx->fs_gptr.p, ctx->fs_gcols.p, m,
+                                                     ctx->fs_tmap.p);
     RBG_CHECK_LAUNCH(ctx);
     RBG_CUDA(cudaStreamSynchronize(st));  // temporaries are released at scope end
     ctx->fs_rho = rho;
-    ctx->fs_nmax = nmax;
     ctx->fs_nnz = nnz;
     ctx->fs_built = true;
 }
 
-struct FsaiLaunch {
-    int warps;
-    uint32_t smem, rowcap;
-    unsigned grid;
-};
-
-template <int MAXT>
-FsaiLaunch fsai_plan_t(rbg_ctx* ctx) {
-    FsaiLaunch L{};
-    L.rowcap = (ctx->max_full_row + 31u) & ~31u;
-    const uint32_t region = fsai_region(ctx->fs_nmax, L.rowcap);
-    // warps per CTA (<= 4) that puts the most warps on an SM (227 KB, 1 KB reserved per CTA)
-    int best = 0;
-    L.warps = 1;
-    for (int w = 1; w <= 4; ++w) {
-        const uint32_t per_cta = region * (uint32_t)w + 1024u;
-        const int on_sm = per_cta <= 227u * 1024u ? (int)((227u * 1024u) / per_cta) * w : 0;
-        if (on_sm > best) {
-            best = on_sm;
-            L.warps = w;
-        }
-    }
-    L.smem = region * (uint32_t)L.warps;
-    RBG_CUDA(cudaFuncSetAttribute(fsai_setup_kernel<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
-    L.grid = resident_grid(ctx, fsai_setup_kernel<MAXT>, blocks_for(ctx->m, (unsigned)L.warps, ~0u), L.smem,
-                           L.warps * 32);
-    return L;
-}
-
+// G for the current values and shift, and its transposed copy (once per ridge attempt).
 void fsai_setup(rbg_ctx* ctx, cudaStream_t st) {
-    const int T = (int)((ctx->fs_nmax + 31u) / 32u);
-    auto go = [&](auto kern, const FsaiLaunch& L) {
-        kern<<<L.grid, L.warps * 32, L.smem, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->vfull.p, ctx->fs_gptr.p,
-                                                   ctx->fs_gcols.p, ctx->m, ctx->fs_nmax, L.rowcap, ctx->bj_perm.p,
-                                                   ctx->scal.p, ctx->fs_gvals.p);
-    };
-    switch (T) {
-        case 0:
-        case 1: go(fsai_setup_kernel<1>, fsai_plan_t<1>(ctx)); break;
-        case 2: go(fsai_setup_kernel<2>, fsai_plan_t<2>(ctx)); break;
-        case 3: go(fsai_setup_kernel<3>, fsai_plan_t<3>(ctx)); break;
-        default: go(fsai_setup_kernel<kFsaiMaxT>, fsai_plan_t<kFsaiMaxT>(ctx)); break;
-    }
+    const uint32_t rowcap = (ctx->max_full_row + 31u) & ~31u;
+    const size_t smem = fsai_setup_smem(rowcap);
+    RBG_CUDA(cudaFuncSetAttribute(fsai_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = resident_grid(ctx, fsai_setup_kernel, blocks_for(ctx->m, kFsaiWarps, ~0u), smem,
+                                        kFsaiWarps * 32);
+    fsai_setup_kernel<<<grid, kFsaiWarps * 32, smem, st>>>(ctx->pfptr.p, ctx->pfcols.p, ctx->vfull.p, ctx->fs_gptr.p,
+                                                           ctx->fs_gcols.p, ctx->m, rowcap, ctx->bj_perm.p,
+                                                           ctx->scal.p, ctx->fs_gvals.p);
     RBG_CHECK_LAUNCH(ctx);
     fsai_transpose_kernel<<<blocks_for(ctx->fs_nnz, kThreads), kThreads, 0, st>>>(ctx->fs_tmap.p, ctx->fs_gvals.p,
                                                                                   ctx->fs_nnz, ctx->fs_tvals.p,
