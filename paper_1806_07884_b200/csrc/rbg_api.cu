@@ -8,6 +8,8 @@
 
 #include <cstdlib>
 #include <exception>
+#include <atomic>
+#include <chrono>
 #include <thread>
 
 #include "rbg_internal.cuh"
@@ -262,10 +264,10 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
         if (n > 0 && (!points || !h)) throw Error(RBG_INVALID_ARGUMENT, "null point or value array");
         bind(ctx);
         const int dim = ctx->dim;
-        // Large pinned inputs are uploaded in chunks on a
-        // copy stream, each chunk assembled (accumulating) as soon as it has
-        // landed, so the upload overlaps the binning and assembly of the chunks
-        // before it.  Pageable inputs go through the staging ring in one piece.
+        // Large inputs are uploaded in chunks on a copy stream (pinned: direct
+        // copies; pageable: through the staging ring), each chunk assembled
+        // (accumulating) as soon as it has landed, so the upload overlaps the
+        // binning and assembly of the chunks before it.
         static const int chunks_env = [] {
             const char* e = std::getenv("RBG_H2D_CHUNKS");
             return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
@@ -283,37 +285,60 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
             if (n > 0 && n * dim * sizeof(double) >= (size_t{64} << 20) && !rbg::page_locked(points)) {
                 // large pageable inputs: the staged upload (host copy threads + the copy
                 // engine, on the copy stream) overlaps the centre-side setup of this context
-                // -- tile grid, pattern and assembly layout, on the compute stream
+                // -- tile grid, pattern, assembly layout and the solver's structures, on the
+                // compute stream -- and, with RBG_H2D_CHUNKS, the assembly of the chunks that
+                // have already landed
                 if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
                 if (!ctx->chunk_ev[0]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
                 RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->stream));  // earlier readers of in_pts / in_h
                 RBG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
+                const int KP = chunks_env ? chunks_env : 1;  // measured: chunking a staged upload does not pay (cfg5 273 vs 260-340 ms)
+                std::vector<uint64_t> off(KP + 1);
+                for (int c = 0; c <= KP; ++c) off[c] = n * (uint64_t)c / (uint64_t)KP;
+                std::atomic<int> landed{0};
                 std::exception_ptr up_err;
                 std::thread up([&] {
                     try {
                         RBG_CUDA(cudaSetDevice(ctx->device));
-                        rbg::h2d_on(ctx->copy_stream, ctx->in_pts.p, points, n * dim * sizeof(double));
-                        rbg::h2d_on(ctx->copy_stream, ctx->in_h.p, h, n * sizeof(double));
+                        for (int c = 0; c < KP; ++c) {  // h2d_on returns once the chunk is on the device
+                            const uint64_t a = off[c], len = off[c + 1] - a;
+                            rbg::h2d_on(ctx->copy_stream, ctx->in_pts.p + a * dim, points + a * dim,
+                                        len * dim * sizeof(double));
+                            rbg::h2d_on(ctx->copy_stream, ctx->in_h.p + a, h + a, len * sizeof(double));
+                            landed.store(c + 1, std::memory_order_release);
+                        }
                     } catch (...) {
                         up_err = std::current_exception();
+                        landed.store(KP, std::memory_order_release);
                     }
                 });
                 try {
                     require_pattern(ctx);
                     if (!ctx->lay.built) rbg::build_layout(ctx, n);
+                    rbg::prepare_solver(ctx);
+                    for (int c = 0; c < KP; ++c) {
+                        while (landed.load(std::memory_order_acquire) <= c)
+                            std::this_thread::sleep_for(std::chrono::microseconds(100));
+                        if (up_err) break;
+                        const uint64_t a = off[c], len = off[c + 1] - a;
+                        if (validate) {
+                            const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p + a * dim, len, dim);
+                            if (bad < len) {
+                                ctx->have_system = false;
+                                throw Error(RBG_INVALID_ARGUMENT,
+                                            "non-finite coordinate at point index " + std::to_string(a + bad));
+                            }
+                        }
+                        rbg::assemble_points(ctx, ctx->in_pts.p + a * dim, ctx->in_h.p + a, len,
+                                             accumulate != 0 || c > 0);
+                    }
                 } catch (...) {
                     up.join();
                     throw;
                 }
                 up.join();
                 if (up_err) std::rethrow_exception(up_err);
-                RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->copy_stream));
-                RBG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[0], 0));
-                if (validate) {
-                    const uint64_t bad = rbg::first_nonfinite(ctx, ctx->in_pts.p, n, dim);
-                    if (bad < n)
-                        throw Error(RBG_INVALID_ARGUMENT, "non-finite coordinate at point index " + std::to_string(bad));
-                }
+                return;
             } else if (n > 0) {
                 require_pattern(ctx);
                 rbg::h2d(ctx, ctx->in_pts.p, points, n * dim * sizeof(double));

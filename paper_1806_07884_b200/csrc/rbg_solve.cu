@@ -935,14 +935,37 @@ void fsai_setup(rbg_ctx* ctx, cudaStream_t st) {
 
 }  // namespace
 
-void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rbg_solve_diag* diag) {
-    // method: FSAI-preconditioned CG unless the caller (rbg_solve_options::method)
-    // or RBG_SOLVER=pcg / band asks for the banded LLT of rbg_band.cu, the
-    // reference's own factorisation (tests, A/B)
+namespace {
+int solver_env() {  // RBG_SOLVER=pcg / band forces a method (tests, A/B)
     static const int forced = [] {
         const char* e = std::getenv("RBG_SOLVER");
         return !e ? 0 : std::string(e) == "pcg" ? RBG_SOLVE_PCG : std::string(e) == "band" ? RBG_SOLVE_BAND : 0;
     }();
+    return forced;
+}
+int prec_env() {  // RBG_PREC=jacobi / fsai forces a preconditioner
+    static const int forced = [] {
+        const char* e = std::getenv("RBG_PREC");
+        return !e ? 0 : std::string(e) == "jacobi" ? RBG_PREC_JACOBI : std::string(e) == "fsai" ? RBG_PREC_FSAI : 0;
+    }();
+    return forced;
+}
+}  // namespace
+
+// The centre-side structures of the default solve (Morton order, permuted CSR,
+// FSAI pattern), built ahead of the first solve where that is free: rbg_assemble
+// calls this while a large host input is still uploading.
+void prepare_solver(rbg_ctx* ctx) {
+    if (ctx->pterms() != 0 || solver_env() == RBG_SOLVE_BAND || prec_env() == RBG_PREC_JACOBI) return;
+    if (!ctx->bj_built) build_solve_order(ctx);
+    if (!ctx->fs_built) fsai_build(ctx);
+}
+
+void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rbg_solve_diag* diag) {
+    // method: FSAI-preconditioned CG unless the caller (rbg_solve_options::method)
+    // or the environment asks for the banded LLT of rbg_band.cu, the reference's
+    // own factorisation
+    const int forced = solver_env();
     const int method = forced ? forced : (opts ? opts->method : 0);
     if (method == RBG_SOLVE_BAND) {
         if (ctx->pterms() != 0)
@@ -984,11 +1007,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
 
     // preconditioner: FSAI (in the Morton order of the centres) unless the caller
     // or RBG_PREC=jacobi asks for point Jacobi, or the system is bordered
-    static const int prec_env = [] {
-        const char* e = std::getenv("RBG_PREC");
-        return !e ? 0 : std::string(e) == "jacobi" ? RBG_PREC_JACOBI : std::string(e) == "fsai" ? RBG_PREC_FSAI : 0;
-    }();
-    const int prec = prec_env ? prec_env : (opts ? opts->precond : 0);
+    const int prec = prec_env() ? prec_env() : (opts ? opts->precond : 0);
     const bool fsai = prec != RBG_PREC_JACOBI && T == 0;
     if (fsai && !ctx->bj_built) build_solve_order(ctx);
     if (fsai && !ctx->fs_built) fsai_build(ctx);
