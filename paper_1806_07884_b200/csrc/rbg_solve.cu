@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
 #pragma unroll
         for (int j = 0; j < kFsaiN; ++j) row[j] = S[lane][j];
         bool bad = false;
+        double myinv = 1.0;
 #pragma unroll
         for (int j = 0; j < kFsaiN; ++j) {
             double d = __shfl_sync(0xffffffffu, row[j], j);
@@ -748,6 +749,7 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
                 d = 1.0;
             }
             const double inv = rsqrt(d);
+            if (lane == j) myinv = inv;      // 1 / L[j][j] for the solve below
             const double lj = row[j] * inv;  // column j of L (rows >= j; lane j: sqrt(d))
             row[j] = lj;
 #pragma unroll
@@ -768,11 +770,40 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
             double t = lane > i ? x * row[i] : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == i) x = ((i == n - 1 ? 1.0 : 0.0) - t) / row[i];
+            if (lane == i) x = ((i == n - 1 ? 1.0 : 0.0) - t) * myinv;
         }
         if (lane < n) gvals[g0 + lane] = x;
         __syncwarp();
     }
+}
+
+// Rows of G and G^T hold about 32 entries, so the applies give a row to a
+// group of 8 lanes (4 rows per warp, 3 shuffle steps per row sum).
+constexpr int kRowLanes = 8;
+constexpr int kRowsPerWarp = 32 / kRowLanes;
+
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = kRowLanes / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double sparse_row_dot(const uint64_t* __restrict__ ptr, const uint32_t* __restrict__ cols,
+                                                 const double* __restrict__ vals, uint64_t row, bool valid, int sl,
+                                                 const double* __restrict__ x) {
+    double s0 = 0.0, s1 = 0.0;
+    if (valid) {
+        const uint64_t e1 = ptr[row + 1];
+        uint64_t e = ptr[row] + sl;
+        for (; e + kRowLanes < e1; e += 2 * kRowLanes) {
+            const uint32_t c0 = __ldcs(cols + e), c1 = __ldcs(cols + e + kRowLanes);
+            const double v0 = __ldcs(vals + e), v1 = __ldcs(vals + e + kRowLanes);
+            s0 = fma(v0, x[c0], s0);
+            s1 = fma(v1, x[c1], s1);
+        }
+        if (e < e1) s0 = fma(__ldcs(vals + e), x[__ldcs(cols + e)], s0);
+    }
+    return group_sum(s0 + s1);
 }
 
 // u = G r, rz = u.u (= r.M^-1 r); INIT: scal[S_RZ] = rz, else beta = rz / rz_old.
@@ -783,22 +814,14 @@ __global__ void __launch_bounds__(kThreads) fsai_lower_kernel(const uint64_t* __
                                                               const double* __restrict__ r, double* __restrict__ u,
                                                               double* partials, unsigned* ticket, double* scal) {
     if (scal[S_FAIL] != 0.0 || (!INIT && scal[S_DONE] != 0.0)) return;
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
+    const int lane = threadIdx.x & 31, sub = lane / kRowLanes, sl = lane % kRowLanes;
+    const uint64_t stride = (uint64_t)gridDim.x * (kThreads / 32) * kRowsPerWarp;
     double v[1] = {0.0};
-    for (uint64_t row = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < m; row += warps) {
-        const uint64_t e1 = gptr[row + 1];
-        double s0 = 0.0, s1 = 0.0;
-        uint64_t e = gptr[row] + lane;
-        for (; e + 32 < e1; e += 64) {
-            const uint32_t c0 = __ldcs(gcols + e), c1 = __ldcs(gcols + e + 32);
-            const double v0 = __ldcs(gvals + e), v1 = __ldcs(gvals + e + 32);
-            s0 = fma(v0, r[c0], s0);
-            s1 = fma(v1, r[c1], s1);
-        }
-        if (e < e1) s0 = fma(__ldcs(gvals + e), r[__ldcs(gcols + e)], s0);
-        const double s = warp_sum(s0 + s1);
-        if (lane == 0) {
+    for (uint64_t base = ((uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * kRowsPerWarp; base < m;
+         base += stride) {
+        const uint64_t row = base + sub;
+        const double s = sparse_row_dot(gptr, gcols, gvals, row, row < m, sl, r);
+        if (sl == 0 && row < m) {
             u[row] = s;
             v[0] += s * s;
         }
@@ -819,21 +842,13 @@ __global__ void __launch_bounds__(kThreads) fsai_upper_kernel(const uint64_t* __
                                                               const double* scal) {
     if (scal[S_FAIL] != 0.0 || (!INIT && scal[S_DONE] != 0.0)) return;
     const double beta = INIT ? 0.0 : scal[S_BETA];
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = (uint64_t)gridDim.x * (kThreads / 32);
-    for (uint64_t row = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); row < m; row += warps) {
-        const uint64_t e1 = tptr[row + 1];
-        double s0 = 0.0, s1 = 0.0;
-        uint64_t e = tptr[row] + lane;
-        for (; e + 32 < e1; e += 64) {
-            const uint32_t c0 = __ldcs(tcols + e), c1 = __ldcs(tcols + e + 32);
-            const double v0 = __ldcs(tvals + e), v1 = __ldcs(tvals + e + 32);
-            s0 = fma(v0, u[c0], s0);
-            s1 = fma(v1, u[c1], s1);
-        }
-        if (e < e1) s0 = fma(__ldcs(tvals + e), u[__ldcs(tcols + e)], s0);
-        const double s = warp_sum(s0 + s1);
-        if (lane == 0) p[row] = INIT ? s : fma(beta, p[row], s);
+    const int lane = threadIdx.x & 31, sub = lane / kRowLanes, sl = lane % kRowLanes;
+    const uint64_t stride = (uint64_t)gridDim.x * (kThreads / 32) * kRowsPerWarp;
+    for (uint64_t base = ((uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * kRowsPerWarp; base < m;
+         base += stride) {
+        const uint64_t row = base + sub;
+        const double s = sparse_row_dot(tptr, tcols, tvals, row, row < m, sl, u);
+        if (sl == 0 && row < m) p[row] = INIT ? s : fma(beta, p[row], s);
     }
 }
 
@@ -1034,7 +1049,8 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     for (int t = 0; t < T; ++t) trace += hF[t * T + t];
     const double mean_diag = trace / (double)nt;  // solver.cpp:296 (trace / side)
 
-    const unsigned g_fs = fsai ? resident_grid(ctx, fsai_lower_kernel<false>, blocks_for(m, kThreads / 32, ~0u)) : 0u;
+    const unsigned g_fs =
+        fsai ? resident_grid(ctx, fsai_lower_kernel<false>, blocks_for(m, kThreads / 32 * kRowsPerWarp, ~0u)) : 0u;
     if (fsai) ctx->partials.reserve(4ull * std::max({g_vec, g_spmv, g_fs}));
 
     // one batch of iterations as a graph (kernels read their scalars on device);
