@@ -169,6 +169,7 @@ def datagen() -> C.CDLL:
         L.dg_sincos.argtypes = [_P, _U64, _P]
         L.dg_bump3.argtypes = [_P, _U64, _P]
         L.dg_mixture.argtypes = [_U64, _U64, _P]
+        L.dg_mixture_floor.argtypes = [_U64, _U64, C.c_int, _P]
         L.dg_fbm.argtypes = [_U64, _P, _U64, _P]
         for f in ("dg_halton", "dg_halton_strided", "dg_add_noise_strided", "dg_grid_refs", "dg_franke", "dg_uniform", "dg_add_noise",
                   "dg_sincos", "dg_bump3", "dg_mixture", "dg_fbm"):

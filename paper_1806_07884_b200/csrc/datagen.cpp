@@ -157,8 +157,13 @@ void dg_bump3(const double* xyz, uint64_t n, double* out) {
 
 // config 4 points: 4 isotropic Gaussians (sigma 0.05-0.2) plus a 5% uniform
 // floor (keeps every Halton centre's support populated), clamped to [0,1]^2.
-void dg_mixture(uint64_t seed, uint64_t n, double* out) {
-    static const double w[5] = {0.30, 0.25, 0.25, 0.15, 0.05};
+// floor = 0 draws BASELINE's pure 4-Gaussian mixture (the same component
+// weights renormalised), used to measure the assembly both ways.
+void dg_mixture_floor(uint64_t seed, uint64_t n, int floor, double* out);
+void dg_mixture(uint64_t seed, uint64_t n, double* out) { dg_mixture_floor(seed, n, 1, out); }
+void dg_mixture_floor(uint64_t seed, uint64_t n, int floor, double* out) {
+    const double f = floor ? 1.0 : 1.0 / 0.95;
+    const double w[5] = {0.30 * f, 0.25 * f, 0.25 * f, floor ? 0.15 : 2.0, 0.05};
     static const double mx[4] = {0.30, 0.70, 0.50, 0.20};
     static const double my[4] = {0.30, 0.35, 0.75, 0.80};
     static const double sg[4] = {0.05, 0.10, 0.20, 0.08};

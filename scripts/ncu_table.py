@@ -28,6 +28,16 @@ for r in rows[2:]:
         u = units[col[k]] if k in col else ""
         sc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}.get(u, 1.0)
         return f(k, sc)
+    def dram_pct(r, tscale, peak_gbs=6547.2):  # (read + write) / time against MEASURED_PEAKS.json hbm_gbs
+        try:
+            tot = 0.0
+            for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                u = units[col[k]]
+                tot += float(g(r, k).replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1.0)
+            us = float(g(r, "gpu__time_duration.sum").replace(",", "")) * tscale
+            return "{:.1f}".format(100.0 * tot / (us * 1e-6) / (peak_gbs * 1e9))
+        except (ValueError, KeyError, ZeroDivisionError):
+            return "-"
     st = [(h, r[i]) for h, i in col.items() if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")]
     tot = sum(float(v or 0) for _, v in st) or 1.0
     top = ", ".join(f"{h.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * float(v or 0) / tot:.0f}%"
@@ -36,4 +46,4 @@ for r in rows[2:]:
           f"{g(r, 'launch__registers_per_thread')} | {f('sm__warps_active.avg.pct_of_peak_sustained_active')} | "
           f"{f('smsp__issue_active.avg.pct_of_peak_sustained_active')} | {f('sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active')} | "
           f"{f('sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active')} | {mb('dram__bytes_read.sum')} | {mb('dram__bytes_write.sum')} | "
-          f"{f('dram__throughput.avg.pct_of_peak_sustained_elapsed')} | {top} |")
+          f"{dram_pct(r, tscale)} | {top} |")

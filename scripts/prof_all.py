@@ -19,7 +19,7 @@ with api.Engine(0) as e:
     e.evaluate(c, xy[:1_000_000])
     e.error_report(c, xy[:1_000_000], h[:1_000_000])
     try:  # solver kernels last (ncu -c truncates the repeated iterations)
-        e.solve(max_iter=40)
+        e.solve(max_iter=12)
     except Exception as ex:  # 40 iterations do not converge: only the kernels matter here
         print("solve:", str(ex)[:80])
 with api.Engine(0) as e:
