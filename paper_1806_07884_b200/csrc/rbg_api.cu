@@ -76,11 +76,17 @@ void check_points_finite(const double* p, uint64_t n, int dim, const char* what)
 }
 
 void check_misses(rbg_ctx* ctx) {
-    unsigned long long miss = 0;
-    RBG_CUDA(cudaMemcpyAsync(&miss, ctx->counters.p, sizeof(miss), cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long c[8] = {};
+    RBG_CUDA(cudaMemcpyAsync(c, ctx->counters.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     RBG_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (miss)
-        throw Error(RBG_RUNTIME_ERROR, "internal: " + std::to_string(miss) +
+    if (c[7]) {  // the dense-centre fallback path keeps 512 hits per point
+        RBG_CUDA(cudaMemsetAsync(ctx->counters.p + 7, 0, sizeof(unsigned long long), ctx->stream));
+        ctx->have_system = false;
+        throw Error(RBG_INVALID_ARGUMENT, std::to_string(c[7]) + " points lie in the support of more than 512 "
+                                          "centres of a dense centre cluster; reduce the support radius");
+    }
+    if (c[0])
+        throw Error(RBG_RUNTIME_ERROR, "internal: " + std::to_string(c[0]) +
                                            " assembly updates fell outside the symbolic pattern");
 }
 
