@@ -489,7 +489,7 @@ void build_solve_order(rbg_ctx* ctx) {
     len.reserve(m + 1);
     ctx->pfptr.reserve(m + 1);
     ctx->puptr.reserve(m);
-    ctx->pfcols.reserve(ctx->nnz_full);
+    ctx->pfcols.reserve(ctx->nnz_full + 4);  // the FSAI row staging reads whole 16-byte pieces
     ctx->pf2u.reserve(ctx->nnz_full);
     perm_len_kernel<<<blocks_for(m, 256), 256, 0, st>>>(ctx->fptr.p, ctx->uptr.p, ctx->bj_perm.p, m, len.p,
                                                        ctx->puptr.p);
@@ -667,9 +667,10 @@ __global__ void fsai_transpose_kernel(const uint32_t* __restrict__ tmap, const d
 //             ascending: binary search) and files B[P[a], P[b]] into S[a][b]
 //             in shared memory, from where lane a takes its row;
 //  factorise  right-looking Cholesky of the 32 x 32 system with row a in the
-//             registers of lane a: per column one pivot broadcast and one
-//             shuffle + FMA per trailing column (rows past n are identity);
-//  solve      x^T L = e_n^T from the last row up: x = row k of G.
+//             registers of lane a: per column one pivot broadcast, the column
+//             parked in shared memory, one broadcast load + FMA per trailing
+//             column (rows past n are identity);
+//  solve      L^T x = e_n from the last row up: x = row k of G.
 constexpr int kFsaiStages = 4;  // row buffers in flight per warp (cp.async)
 inline size_t fsai_setup_smem(uint32_t rowcap) {
     return (size_t)kFsaiWarps * (kFsaiN * (kFsaiN + 1) * sizeof(double) + (size_t)kFsaiStages * rowcap * sizeof(uint32_t));
@@ -696,13 +697,14 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
         // the columns of B's row P[a] -> row buffer a % kFsaiStages (asynchronous)
         const auto issue_row = [&](int a) {
             if (a < n) {
+                // 16-byte pieces from the row start rounded down to a multiple of 4 entries
+                // (the row then begins at offset e0 & 3 of the buffer)
                 const uint64_t e0 = __shfl_sync(0xffffffffu, my0, a);
-                const uint32_t len = __shfl_sync(0xffffffffu, mylen, a);
-                uint32_t* dst = rbuf + (a % kFsaiStages) * rowcap;
-                for (uint32_t e = lane; e < len; e += 32)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(dst + e)),
-                                 "l"(pfcols + e0 + e)
+                const uint32_t len = __shfl_sync(0xffffffffu, mylen, a) + (uint32_t)(e0 & 3);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rbuf + (a % kFsaiStages) * rowcap);
+                const uint32_t* src = pfcols + (e0 & ~3ull);
+                for (uint32_t e = 4 * lane; e < len; e += 128)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 4u * e), "l"(src + e)
                                  : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -722,7 +724,7 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
             __syncwarp();
             const uint64_t e0 = __shfl_sync(0xffffffffu, my0, a);
             const uint32_t len = __shfl_sync(0xffffffffu, mylen, a);
-            const uint32_t* rc = rbuf + (a % kFsaiStages) * rowcap;
+            const uint32_t* rc = rbuf + (a % kFsaiStages) * rowcap + (e0 & 3);
             uint32_t lo = 0;
             for (uint32_t step = 1u << (31 - __clz(len)); step > 0; step >>= 1)
                 if (lo + step <= len && rc[lo + step - 1] < mine) lo += step;
@@ -739,21 +741,30 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
         double row[kFsaiN];
 #pragma unroll
         for (int j = 0; j < kFsaiN; ++j) row[j] = S[lane][j];
+        __syncwarp();
+        // S is reused for L, column-major (Lc[j][i] = L[i][j]): every finished column is
+        // parked there, the trailing update reads it back as broadcasts (one LDS per
+        // column instead of a two-instruction 64-bit shuffle) and the solve below walks it
+        double* Lc = &S[0][0];
+        constexpr int LD = kFsaiN + 1;
         bool bad = false;
         double myinv = 1.0;
 #pragma unroll
         for (int j = 0; j < kFsaiN; ++j) {
-            double d = __shfl_sync(0xffffffffu, row[j], j);
-            if (!(d > 0.0) || !isfinite(d)) {
-                bad = true;
-                d = 1.0;
-            }
-            const double inv = rsqrt(d);
-            if (lane == j) myinv = inv;      // 1 / L[j][j] for the solve below
-            const double lj = row[j] * inv;  // column j of L (rows >= j; lane j: sqrt(d))
-            row[j] = lj;
+            if (j < n) {  // rows past n are identity
+                double d = __shfl_sync(0xffffffffu, row[j], j);
+                if (!(d > 0.0) || !isfinite(d)) {
+                    bad = true;
+                    d = 1.0;
+                }
+                const double inv = rsqrt(d);
+                if (lane == j) myinv = inv;      // 1 / L[j][j] for the solve below
+                const double lj = row[j] * inv;  // column j of L (rows >= j; lane j: sqrt(d))
+                Lc[j * LD + lane] = lj;
+                __syncwarp();
 #pragma unroll
-            for (int c = j + 1; c < kFsaiN; ++c) row[c] = fma(-lj, __shfl_sync(0xffffffffu, lj, c), row[c]);
+                for (int c = j + 1; c < kFsaiN; ++c) row[c] = fma(-lj, Lc[j * LD + c], row[c]);
+            }
         }
         if (bad) {
             if (lane == 0) {
@@ -761,16 +772,15 @@ __global__ void __launch_bounds__(kFsaiWarps * 32) fsai_setup_kernel(
                 atomicMin(reinterpret_cast<unsigned long long*>(scal + S_PIV),
                           (unsigned long long)__double_as_longlong((double)perm[k]));
             }
+            __syncwarp();
             continue;
         }
-        // x_i = ([i == n - 1] - sum_{i' > i} x_i' L[i'][i]) / L[i][i]
-        double x = 0.0;
-#pragma unroll
-        for (int i = kFsaiN - 1; i >= 0; --i) {
-            double t = lane > i ? x * row[i] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == i) x = ((i == n - 1 ? 1.0 : 0.0) - t) * myinv;
+        // L^T x = e_{n-1}, column by column: once x_i is final, row i of L updates x_0 .. x_{i-1}
+        double x = lane == n - 1 ? 1.0 : 0.0;
+        for (int i = n - 1; i >= 0; --i) {
+            if (lane == i) x *= myinv;
+            const double xi = __shfl_sync(0xffffffffu, x, i);
+            if (lane < i) x = fma(-Lc[lane * LD + i], xi, x);
         }
         if (lane < n) gvals[g0 + lane] = x;
         __syncwarp();
@@ -933,7 +943,7 @@ void fsai_build(rbg_ctx* ctx) {
 
 // G for the current values and shift, and its transposed copy (once per ridge attempt).
 void fsai_setup(rbg_ctx* ctx, cudaStream_t st) {
-    const uint32_t rowcap = (ctx->max_full_row + 31u) & ~31u;
+    const uint32_t rowcap = (ctx->max_full_row + 3u + 31u) & ~31u;  // + the alignment shift of a staged row
     const size_t smem = fsai_setup_smem(rowcap);
     RBG_CUDA(cudaFuncSetAttribute(fsai_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = resident_grid(ctx, fsai_setup_kernel, blocks_for(ctx->m, kFsaiWarps, ~0u), smem,
@@ -970,8 +980,13 @@ int prec_env() {  // RBG_PREC=jacobi / fsai forces a preconditioner
 // The centre-side structures of the default solve (Morton order, permuted CSR,
 // FSAI pattern), built ahead of the first solve where that is free: rbg_assemble
 // calls this while a large host input is still uploading.
+// The FSAI kernels stage whole rows of B in shared memory; beyond 1024 entries
+// per row (hundreds of centres per support -- far outside the method's regime)
+// the solve keeps point Jacobi.
+bool fsai_fits(const rbg_ctx* ctx) { return ctx->max_full_row <= 1024u; }
+
 void prepare_solver(rbg_ctx* ctx) {
-    if (ctx->pterms() != 0 || solver_env() == RBG_SOLVE_BAND || prec_env() == RBG_PREC_JACOBI) return;
+    if (ctx->pterms() != 0 || solver_env() == RBG_SOLVE_BAND || prec_env() == RBG_PREC_JACOBI || !fsai_fits(ctx)) return;
     if (!ctx->bj_built) build_solve_order(ctx);
     if (!ctx->fs_built) fsai_build(ctx);
 }
@@ -1023,7 +1038,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     // preconditioner: FSAI (in the Morton order of the centres) unless the caller
     // or RBG_PREC=jacobi asks for point Jacobi, or the system is bordered
     const int prec = prec_env() ? prec_env() : (opts ? opts->precond : 0);
-    const bool fsai = prec != RBG_PREC_JACOBI && T == 0;
+    const bool fsai = prec != RBG_PREC_JACOBI && T == 0 && fsai_fits(ctx);
     if (fsai && !ctx->bj_built) build_solve_order(ctx);
     if (fsai && !ctx->fs_built) fsai_build(ctx);
     const uint64_t* s_fptr = fsai ? ctx->pfptr.p : ctx->fptr.p;
