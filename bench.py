@@ -487,6 +487,7 @@ def _e2e(xy, h, refs, kernel, cfg, world, rank, local, args, stream):
     dt = _max_over_ranks(sum(times) / len(times), world)
     n_total = _sum_over_ranks(len(h), world)
     return {"value": n_total / dt, "unit": UNIT, "ms_per_step": dt * 1e3, "steps": steps,
+            "ms_min": min(times) * 1e3, "ms_median": statistics.median(times) * 1e3, "ms_max": max(times) * 1e3,
             "h2d_bytes_per_step": int(len(h) * (cfg.dim + 1) * 8 + refs.size * 8),
             "d2h_bytes_per_step": int(cfg.m * 8 + (cfg.m * 8 if world == 1 else 0)),
             "api": ("api.fit -> rbg_create, rbg_set_centres, rbg_assemble (pageable host arrays, validated), "
