@@ -187,8 +187,13 @@ def test_solver_methods_and_preconditioners_agree(eng):
     system to the same c (<= 1e-8), in 2-D and 3-D; FSAI needs an order of magnitude fewer
     iterations than point Jacobi."""
     rng = np.random.default_rng(11)
-    for dim, m, n, fam, alpha in ((2, 900, 60_000, "wendland-3-1", 6.0), (3, 700, 60_000, "wendland-3-2", 3.0)):
-        refs = rng.random((m, dim))
+    for dim, side, n, fam, per_support in ((2, 30, 60_000, "wendland-3-1", 25.0), (3, 9, 60_000, "wendland-3-2", 30.0)):
+        # jittered grid centres (random ones cluster: point Jacobi then needs > 20000 iterations)
+        g = (np.stack(np.meshgrid(*[np.arange(side)] * dim, indexing="ij"), -1).reshape(-1, dim) + 0.5) / side
+        refs = np.ascontiguousarray(g + (rng.random(g.shape) - 0.5) * 0.3 / side)
+        m = refs.shape[0]
+        r = (per_support / (np.pi * m)) ** 0.5 if dim == 2 else (per_support / (m * 4.0 * np.pi / 3.0)) ** (1.0 / 3.0)
+        alpha = 1.0 / r
         pts = rng.random((n, dim))
         h = np.sin(3.0 * pts[:, 0]) + pts[:, 1] ** 2
         eng.set_centres(refs, api.KernelSpec(fam, alpha))
