@@ -320,7 +320,7 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
                 });
                 try {
                     require_pattern(ctx);
-                    if (!ctx->lay.built) rbg::build_layout(ctx, n);
+                    rbg::ensure_layout(ctx, n);
                     rbg::prepare_solver(ctx);
                     for (int c = 0; c < KP; ++c) {
                         while (landed.load(std::memory_order_acquire) <= c)
@@ -356,11 +356,12 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
                 }
             }
             require_pattern(ctx);  // (no-op when built above)
+            if (n > 0) rbg::ensure_layout(ctx, n);
             rbg::assemble_points(ctx, ctx->in_pts.p, ctx->in_h.p, n, accumulate != 0);
             return;
         }
         require_pattern(ctx);
-        if (!ctx->lay.built) rbg::build_layout(ctx, n);  // tile sizes follow the whole batch's density
+        rbg::ensure_layout(ctx, n);  // tile sizes follow the whole batch's density
         if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
         for (int c = 0; c < K; ++c)
             if (!ctx->chunk_ev[c]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[c], cudaEventDisableTiming));
@@ -398,6 +399,7 @@ rbg_status rbg_assemble_device(rbg_ctx* ctx, const double* d_points, const doubl
     return guarded(ctx, [&] {
         require_pattern(ctx);
         bind(ctx);
+        if (n > 0) rbg::ensure_layout(ctx, n);
         rbg::assemble_points(ctx, d_points, d_h, n, accumulate != 0);
     });
 }

@@ -396,7 +396,18 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     ctx->tile_pptr.reserve(L.n_keys + 1);
     RBG_CUDA(cudaStreamSynchronize(st));
     L.built = true;
+    L.n_built = n_points;
     L.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// The sub-tile size follows the point density, so a layout built for a very
+// different point count (a small first call, then the real one) is rebuilt;
+// explicit rbg_set_tile_divisor / rbg_set_super_factor choices are kept.
+void ensure_layout(rbg_ctx* ctx, uint64_t n_points) {
+    const AsmLayout& L = ctx->lay;
+    const bool pinned_choice = ctx->sub_div_req > 0 || ctx->super_req > 0;
+    if (L.built && (pinned_choice || (n_points <= 4 * L.n_built && L.n_built <= 4 * n_points))) return;
+    build_layout(ctx, n_points);
 }
 
 }  // namespace rbg

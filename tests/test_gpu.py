@@ -181,6 +181,28 @@ def test_empty_support_ridge_and_pivot_message(eng):
         eng.solve()
 
 
+def test_layout_follows_the_point_count(eng):
+    """The assembly tiling is chosen from the point density: a small first call must not pin the
+    layout of a later, much larger one (rbg::ensure_layout), and results do not depend on it."""
+    cfg = configs.CONFIGS["cfg2"]
+    xy, h = configs.points("cfg2", n=400_000)
+    refs = configs.centres("cfg2")
+    k = api.KernelSpec(cfg.kernel, cfg.alpha)
+    with api.Engine(0) as fresh:
+        fresh.set_centres(refs, k)
+        fresh.assemble(xy, h)
+        want = fresh.layout_info()
+        ref_sys = fresh.system()
+    eng.set_centres(refs, k)
+    eng.assemble(xy[:500], h[:500])
+    small = eng.layout_info()
+    eng.assemble(xy, h)
+    got = eng.layout_info()
+    assert (got["sub_div"], got["super_factor"]) == (want["sub_div"], want["super_factor"]), (small, got, want)
+    s = eng.system()
+    assert scaled(s["values"], ref_sys["values"]) < TOL_SYS and np.array_equal(s["hits"], ref_sys["hits"])
+
+
 def test_solver_methods_and_preconditioners_agree(eng):
     """rbg_solve_options::method / precond: the FSAI-preconditioned CG (default), point-Jacobi CG
     and the banded LLT (the reference's factorisation, solver.cpp:289-330) solve the same assembled
