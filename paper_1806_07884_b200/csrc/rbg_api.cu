@@ -23,6 +23,7 @@ rbg_status guarded(rbg_ctx* ctx, F&& f) {
     if (!ctx) return RBG_INVALID_ARGUMENT;
     try {
         ctx->err.clear();
+        rbg::StreamScope scope(ctx->stream);  // temporaries released inside are recycled after draining this stream
         f();
         return RBG_OK;
     } catch (const Error& e) {

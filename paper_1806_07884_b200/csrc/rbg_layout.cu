@@ -346,14 +346,33 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
             lists[smax * nlc + lmax] = std::move(all);
         }
     }
-    const bool lpt = env_int("RBG_LPT", 1) != 0;
-    for (auto& v : lists) {
-        if (lpt)
-            std::sort(v.begin(), v.end(), [&](uint32_t a, uint32_t b) {
-                return weight[a] != weight[b] ? weight[a] > weight[b] : a < b;
-            });
-        else
-            std::sort(v.begin(), v.end());
+    // longest-processing-time order: weight descending, ids ascending within a weight
+    // (a counting sort -- the weights are small integers; 400k super-tiles at cfg5)
+    {
+        uint32_t wmax = 0;
+        for (const uint32_t w : weight) wmax = std::max(wmax, w);
+        std::vector<uint32_t> slot(n_super, 0xffffffffu), start((size_t)wmax + 2, 0), out;
+        for (auto& v : lists) {
+            if (v.size() < 2) continue;
+            std::fill(start.begin(), start.end(), 0u);
+            for (const uint32_t T : v) {
+                slot[T] = wmax - weight[T];  // sort key: 0 = heaviest
+                ++start[slot[T] + 1];
+            }
+            for (size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
+            out.resize(v.size());
+            uint32_t lo = 0xffffffffu, hi = 0;
+            for (const uint32_t T : v) {
+                lo = std::min(lo, T);
+                hi = std::max(hi, T);
+            }
+            for (uint32_t T = lo; T <= hi; ++T)  // ascending ids keep the ties ordered
+                if (slot[T] != 0xffffffffu) {
+                    out[start[slot[T]]++] = T;
+                    slot[T] = 0xffffffffu;
+                }
+            v.swap(out);
+        }
     }
     L.buckets.clear();
     for (int si = 0; si < nsc; ++si)

@@ -3,6 +3,9 @@
 #include <algorithm>
 #include <cstring>
 #include <condition_variable>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -210,6 +213,30 @@ void trim_cache(int device) {
 RecycleScope::RecycleScope() { ++g_recycle_depth; }
 RecycleScope::~RecycleScope() { --g_recycle_depth; }
 
+namespace {
+thread_local cudaStream_t g_scope_stream = nullptr;
+thread_local bool g_scope_on = false;
+}  // namespace
+StreamScope::StreamScope(cudaStream_t st) : prev(g_scope_stream), had(g_scope_on) {
+    g_scope_stream = st;
+    g_scope_on = true;
+}
+StreamScope::~StreamScope() {
+    g_scope_stream = prev;
+    g_scope_on = had;
+}
+
+namespace {
+// RBG_ALLOC_STATS=1: every cudaMalloc / cudaFree that misses the block cache is
+// reported on stderr (diagnostics for stalls of the fresh-context fit).
+void alloc_note(int kind, size_t bytes, std::chrono::steady_clock::time_point t0) {
+    static const bool on = std::getenv("RBG_ALLOC_STATS") != nullptr;
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[rbg alloc] %s %.1f MB %.3f ms\n", kind ? "cudaFree" : "cudaMalloc", bytes / 1048576.0, ms);
+}
+}  // namespace
+
 void* dev_alloc(size_t bytes, size_t* got) {
     int device = 0;
     RBG_CUDA(cudaGetDevice(&device));
@@ -232,7 +259,9 @@ void* dev_alloc(size_t bytes, size_t* got) {
         }
     }
     void* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMalloc(&p, bytes);
+    alloc_note(0, bytes, t0);
     if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
         cudaGetLastError();
         trim_cache(device);
@@ -246,15 +275,32 @@ void* dev_alloc(size_t bytes, size_t* got) {
 
 void dev_free(void* p, size_t bytes) {
     if (!p) return;
-    if (g_recycle_depth > 0 && bytes >= (size_t{1} << 20)) {
+    const bool drained = g_recycle_depth > 0;
+    if ((drained || g_scope_on) && bytes >= (size_t{64} << 10)) {
         int device = 0;
-        if (cudaGetDevice(&device) == cudaSuccess) {
-            std::lock_guard<std::mutex> lk(g_cache_mu);
-            g_cache.push_back({device, bytes, p});
+        // outside a context teardown the block may still be in use by kernels queued on the
+        // calling context's stream (the only stream temporaries are used on): drain it first
+        if (cudaGetDevice(&device) == cudaSuccess && (drained || cudaStreamSynchronize(g_scope_stream) == cudaSuccess)) {
+            std::vector<CachedBlock> evict;
+            {
+                std::lock_guard<std::mutex> lk(g_cache_mu);
+                g_cache.push_back({device, bytes, p});
+                // bounded: beyond 64 GB (or 4096 blocks) the oldest blocks go back to the driver
+                size_t total = 0;
+                for (const CachedBlock& c : g_cache) total += c.bytes;
+                while (!g_cache.empty() && (total > (size_t{64} << 30) || g_cache.size() > 4096)) {
+                    total -= g_cache.front().bytes;
+                    evict.push_back(g_cache.front());
+                    g_cache.erase(g_cache.begin());
+                }
+            }
+            for (const CachedBlock& c : evict) cudaFree(c.p);
             return;
         }
     }
+    const auto t0 = std::chrono::steady_clock::now();
     cudaFree(p);
+    alloc_note(1, bytes, t0);
 }
 
 // ------------------------------------------------------- staged host copies
