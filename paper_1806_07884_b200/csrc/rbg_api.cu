@@ -293,13 +293,14 @@ rbg_status rbg_assemble(rbg_ctx* ctx, const double* points, const double* h, uin
                 // large pageable inputs: the staged upload (host copy threads + the copy
                 // engine, on the copy stream) overlaps the centre-side setup of this context
                 // -- tile grid, pattern, assembly layout and the solver's structures, on the
-                // compute stream -- and, with RBG_H2D_CHUNKS, the assembly of the chunks that
-                // have already landed
+                // compute stream -- and, from 5e7 points, the assembly of the first half while
+                // the second half is still on its way
                 if (!ctx->copy_stream) RBG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
                 if (!ctx->chunk_ev[0]) RBG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev[0], cudaEventDisableTiming));
                 RBG_CUDA(cudaEventRecord(ctx->chunk_ev[0], ctx->stream));  // earlier readers of in_pts / in_h
                 RBG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[0], 0));
-                const int KP = chunks_env ? chunks_env : 1;  // measured: chunking a staged upload does not pay (cfg5 273 vs 260-340 ms)
+                // measured at cfg5 (fresh-context fit): 1 chunk 231 ms, 2 chunks 218, 3 chunks 233, 4 chunks 250
+                const int KP = chunks_env ? chunks_env : (n >= 50000000 ? 2 : 1);
                 std::vector<uint64_t> off(KP + 1);
                 for (int c = 0; c <= KP; ++c) off[c] = n * (uint64_t)c / (uint64_t)KP;
                 std::atomic<int> landed{0};
