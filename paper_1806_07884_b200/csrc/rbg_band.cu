@@ -445,6 +445,7 @@ void band_solve(rbg_ctx* ctx, double* c_out, rbg_solve_diag* diag) {
     band_permute_kernel<false><<<blocks_for(padded, 256), 256, 0, st>>>(P.perm.p, m, padded, ctx->q.p, ctx->x.p);
     RBG_CHECK_LAUNCH(ctx);
     RBG_CUDA(cudaMemsetAsync(ctx->scal.p, 0, 2 * sizeof(double), st));
+    ensure_f2u(ctx);
     band_residual_kernel<<<blocks_for(m * 32, 256), 256, 0, st>>>(ctx->fptr.p, ctx->fcols.p, ctx->f2u.p, uvals, rhs,
                                                                   ctx->x.p, m, ctx->scal.p);
     RBG_CHECK_LAUNCH(ctx);

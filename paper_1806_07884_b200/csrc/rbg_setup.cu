@@ -421,7 +421,8 @@ void setup_pattern(rbg_ctx* ctx) {
     const double cinv = 1.0 / cedge;
     CellDev cd{lo[0], lo[1], lo[2], cinv, cn[0], cn[1], cn[2]};
     DevBuf<uint64_t> d_cell_ptr;
-    DevBuf<uint32_t> d_cell_ids, d_len, d_diag;
+    DevBuf<uint32_t> d_cell_ids, d_len;
+    DevBuf<uint32_t>& d_diag = ctx->fdiag;  // kept: the full -> upper slot map is built on demand (ensure_f2u)
     d_cell_ptr.reserve(ncell + 1);
     d_cell_ids.reserve(m);
     d_len.reserve(std::max<uint64_t>(m, ncell) + 1);
@@ -477,10 +478,7 @@ void setup_pattern(rbg_ctx* ctx) {
     upper_fill_kernel<<<cb, 128, 0, st>>>(ctx->fptr.p, ctx->fcols.p, m, d_diag.p, ctx->uptr.p,
                                           ctx->ucols.p);
     RBG_CHECK_LAUNCH(ctx);
-    ctx->f2u.reserve(ctx->nnz_full);
-    full_to_upper_kernel<<<cb, 128, 0, st>>>(ctx->fptr.p, ctx->fcols.p, m, d_diag.p, ctx->uptr.p,
-                                             ctx->ucols.p, ctx->f2u.p);
-    RBG_CHECK_LAUNCH(ctx);
+    ctx->have_f2u = false;
 
     // ---- system + point workspace sized for this centre set ----------------
     ctx->sys.reserve(ctx->nnz_upper + 2 * m + 4 * m + 20);  // room for the polynomial border
@@ -488,6 +486,19 @@ void setup_pattern(rbg_ctx* ctx) {
     RBG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
     RBG_CUDA(cudaStreamSynchronize(st));
     ctx->have_pattern = true;
+}
+
+// Full CSR entry -> upper CSR slot, for the solves that run in centre order
+// (point Jacobi, the bordered system, the banded LLT's residual); the default
+// solve carries its own map in Morton order (pf2u) and never needs this one.
+void ensure_f2u(rbg_ctx* ctx) {
+    if (ctx->have_f2u) return;
+    ctx->f2u.reserve(ctx->nnz_full);
+    full_to_upper_kernel<<<blocks_for(ctx->m, 128), 128, 0, ctx->stream>>>(ctx->fptr.p, ctx->fcols.p, ctx->m,
+                                                                           ctx->fdiag.p, ctx->uptr.p, ctx->ucols.p,
+                                                                           ctx->f2u.p);
+    RBG_CHECK_LAUNCH(ctx);
+    ctx->have_f2u = true;
 }
 
 }  // namespace rbg

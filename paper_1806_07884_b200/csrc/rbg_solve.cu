@@ -1045,6 +1045,7 @@ void solve_system(rbg_ctx* ctx, const rbg_solve_options* opts, double* c_out, rb
     const uint32_t* s_fcols = fsai ? ctx->pfcols.p : ctx->fcols.p;
     const uint64_t* s_uptr = fsai ? ctx->puptr.p : ctx->uptr.p;  // diagonal of each solve row
 
+    if (!fsai) ensure_f2u(ctx);
     RBG_CUDA(cudaEventRecord(ctx->ev0, st));
     gather_full_kernel<<<blocks_for(nnz, kThreads), kThreads, 0, st>>>(fsai ? ctx->pf2u.p : ctx->f2u.p, uvals, nnz,
                                                                         ctx->vfull.p);
