@@ -278,7 +278,7 @@ Model fit(const PointCloud& cloud, std::vector<Point2> refs, const KernelSpec& k
     local.assembly_seconds = seconds_since(t0);
     t0 = Clock::now();
     std::vector<double> c(m);
-    rbg_solve_options so{options.tol, options.max_iter, RBG_SOLVE_AUTO, RBG_PREC_AUTO};
+    rbg_solve_options so{options.tol, options.max_iter, options.solve_method, options.preconditioner};
     rbg_solve_diag d{};
     std::optional<std::array<double, 3>> poly;
     const std::size_t unknowns = m + (options.poly ? 3 : 0);

@@ -166,6 +166,8 @@ struct FitOptions {  // solver.hpp:113-118 (+ GPU solve controls)
     std::optional<std::size_t> block_size;  // accepted, unused on the GPU
     double tol = 1e-12;
     int max_iter = 20000;
+    int solve_method = 0;   // rbg.h RBG_SOLVE_*: 0 = FSAI-preconditioned CG, 2 = the reference's LLT on the band
+    int preconditioner = 0; // rbg.h RBG_PREC_*: 0 = automatic (FSAI; point Jacobi with the border)
     int device = 0;
     Device* engine = nullptr;  // the caller's context (and its stream); `device` is then ignored
     AllReduce allreduce;       // multi-GPU: sum partial systems across ranks (see AllReduce)
