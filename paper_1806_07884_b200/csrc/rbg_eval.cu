@@ -15,6 +15,10 @@ namespace rbg {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef RBG_EVAL_BATCH
+#define RBG_EVAL_BATCH 8
+#endif
+constexpr int kEvalBatch = RBG_EVAL_BATCH;  // candidates whose loads are in flight together in eval_kernel
 
 // Linear-polynomial term of a bordered model (model.cpp:65-68): after the
 // support sum, f += a0 x + a1 y (+ a2 z) + a_last, evaluated left to right
@@ -36,8 +40,33 @@ __global__ void eval_kernel(GridDev g, const uint64_t* __restrict__ cptr,
         const uint64_t t = tile_of<DIM>(g, x, y, z);
         double acc = 0.0;
         if (t != ~0ull) {
+            // kEvalBatch candidates at a time: their index, coordinate and weight loads are all in
+            // flight before the first use (the walk is latency-bound: every query of a warp
+            // reads another tile's list); the sum still runs in ascending list order
             const uint64_t e1 = cptr[t + 1];
-            for (uint64_t e = cptr[t]; e < e1; ++e) {
+            uint64_t e = cptr[t];
+            for (; e + kEvalBatch <= e1; e += kEvalBatch) {
+                uint32_t j[kEvalBatch];
+                double cx[kEvalBatch], cy[kEvalBatch], cz[kEvalBatch], wj[kEvalBatch];
+#pragma unroll
+                for (int u = 0; u < kEvalBatch; ++u) j[u] = cids[e + u];
+#pragma unroll
+                for (int u = 0; u < kEvalBatch; ++u) {
+                    cx[u] = centres[(uint64_t)j[u] * DIM];
+                    cy[u] = centres[(uint64_t)j[u] * DIM + 1];
+                    cz[u] = DIM == 3 ? centres[(uint64_t)j[u] * DIM + 2] : 0.0;
+                    wj[u] = w[j[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < kEvalBatch; ++u) {
+                    const double d2 = dist2_of<DIM>(x, y, z, cx[u], cy[u], cz[u]);
+                    if (d2 < r2) {
+                        const double v = phi_of_r(family, alpha, __dsqrt_rn(d2));
+                        if (v != 0.0) acc = __dadd_rn(acc, __dmul_rn(wj[u], v));
+                    }
+                }
+            }
+            for (; e < e1; ++e) {
                 const uint32_t j = cids[e];
                 const double d2 = dist2_of<DIM>(x, y, z, centres[(uint64_t)j * DIM],
                                                 centres[(uint64_t)j * DIM + 1],
