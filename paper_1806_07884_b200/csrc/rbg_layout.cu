@@ -171,7 +171,7 @@ int env_int(const char* name, int dflt) {
 // (about nine 4-point DMMA k-steps per register pass), super-tiles of 2x2
 // sub-tiles, 3x3 from q >= 7 and 4x4 from q >= 9 (larger super-tiles amortise
 // the flush over more points until the accumulator costs occupancy); 3-D: sub-tiles of
-// edge r/2 assembled in direct mode (one sub-tile per super-tile, register
+// about 32 points (edge r/2 .. r/4) assembled in direct mode (one sub-tile per super-tile, register
 // tiles reduced straight into the CSR values: a 3-D super-tile accumulator
 // would not fit shared memory).
 static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* span, int& q, int& S) {
@@ -184,8 +184,9 @@ static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* s
         const double e = std::sqrt(34.0 / rho);
         q = std::max(2, std::min(16, (int)std::lround(r / e)));
         S = q >= 9 ? 4 : q >= 7 ? 3 : 2;
-    } else {
-        q = 2;
+    } else {  // about 32 points per cube (cfg3: r/3, 28 points: K3 5.4 ms; r/2 7.9 ms; r/4 10.6 ms)
+        const double e = std::cbrt(32.0 / rho);
+        q = std::max(2, std::min(4, (int)std::lround(r / e)));
         S = 1;
     }
     // small problems: shrink the super-tiles until there are at least two per
