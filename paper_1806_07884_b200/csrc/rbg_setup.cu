@@ -233,32 +233,52 @@ __global__ void cell_bin_kernel(const double* __restrict__ c, uint64_t m, CellDe
     }
 }
 
-// Per (tile, local row a): merge the tile's ascending list with upper row
-// c_a's ascending columns -> packed slot offsets.
+// Slot maps: per (tile, local row a), the offsets of the tile's columns b >= a within upper
+// row c_a.  A warp takes 32 consecutive rows: every lane resolves its own row (tile by binary
+// search over cptr, CSR row bounds), then the warp walks the 32 rows one at a time, lanes =
+// columns: one binary search per entry in the (L1-resident, few hundred ids) upper row and
+// coalesced 16-bit stores.  (One thread per row merging the two ascending lists: 7-8 ms per
+// call at cfg3 / cfg5, scattered 2-byte stores and divergent trip counts.)
 __global__ void tile_map_kernel(const uint64_t* __restrict__ cptr, uint64_t n_tiles,
                                 const uint32_t* __restrict__ cids, uint64_t total,
                                 const uint64_t* __restrict__ mptr, const uint64_t* __restrict__ uptr,
                                 const uint32_t* __restrict__ ucols, uint16_t* __restrict__ map) {
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        // tile = last t with cptr[t] <= e
-        uint64_t lo = 0, hi = n_tiles;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (cptr[mid] <= e) lo = mid; else hi = mid;
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t e0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32ull; e0 < total;
+         e0 += nw * 32ull) {
+        const uint64_t e = e0 + lane;
+        uint64_t c0 = 0, rb = 0, re = 0, mo = 0;
+        uint32_t L = 0, a = 0;
+        if (e < total) {
+            uint64_t lo = 0, hi = n_tiles;  // tile = last t with cptr[t] <= e
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (cptr[mid] <= e) lo = mid; else hi = mid;
+            }
+            c0 = cptr[lo];
+            L = (uint32_t)(cptr[lo + 1] - c0);
+            a = (uint32_t)(e - c0);
+            const uint32_t ga = cids[e];
+            rb = uptr[ga];
+            re = uptr[ga + 1];
+            mo = mptr[lo] + tri_index(a, a, L);
         }
-        const uint64_t t = lo;
-        const uint64_t c0 = cptr[t];
-        const uint32_t L = (uint32_t)(cptr[t + 1] - c0);
-        const uint32_t a = (uint32_t)(e - c0);
-        const uint32_t ga = cids[e];
-        const uint64_t rb = uptr[ga], re = uptr[ga + 1];
-        uint64_t pos = rb;
-        uint16_t* out = map + mptr[t] + tri_index(a, a, L);
-        for (uint32_t b = a; b < L; ++b) {
-            const uint32_t gb = cids[c0 + b];
-            while (pos < re && ucols[pos] < gb) ++pos;
-            out[b - a] = (pos < re && ucols[pos] == gb) ? (uint16_t)(pos - rb) : (uint16_t)0xffff;
+        const int nrows = (int)(total - e0 < 32ull ? total - e0 : 32ull);
+        for (int r = 0; r < nrows; ++r) {
+            const uint64_t rc0 = __shfl_sync(0xffffffffu, c0, r), rrb = __shfl_sync(0xffffffffu, rb, r);
+            const uint64_t rre = __shfl_sync(0xffffffffu, re, r), rmo = __shfl_sync(0xffffffffu, mo, r);
+            const uint32_t rL = __shfl_sync(0xffffffffu, L, r), ra = __shfl_sync(0xffffffffu, a, r);
+            uint16_t* out = map + rmo;
+            for (uint32_t b = ra + lane; b < rL; b += 32) {
+                const uint32_t gb = cids[rc0 + b];
+                uint64_t l = rrb, h = rre;
+                while (l < h) {
+                    const uint64_t mid = (l + h) >> 1;
+                    if (ucols[mid] < gb) l = mid + 1; else h = mid;
+                }
+                out[b - ra] = (l < rre && ucols[l] == gb) ? (uint16_t)(l - rrb) : (uint16_t)0xffff;
+            }
         }
     }
 }
