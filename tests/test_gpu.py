@@ -125,6 +125,38 @@ def test_config_subsamples(eng, name, n):
     run_and_compare(eng, xy, h, refs, api.KERNELS[cfg.kernel], cfg.alpha if name != "cfg3" else cfg.alpha / 2)
 
 
+@pytest.mark.parametrize("dim,family,m,per_support,n,divisor", [
+    (2, 1, 400, 55, 200_000, 2),    # 2-D, 8-block sub-tiles of ~2000 points: panels 4 + 4, shared accumulator
+    (3, 3, 400, 60, 100_000, 2),    # 3-D direct mode, ~14-block sub-tiles of ~600 points: panels 5 + 5 + 4
+    (3, 2, 300, 70, 40_000, 2),     # 3-D, ~20 blocks: four panels, slot map too large to stage
+])
+def test_multipass_subtiles_in_chunks(dim, family, m, per_support, n, divisor):
+    """Sub-tiles beyond 56 centres are assembled in panels with phi cached in the per-worker
+    scratch, and beyond 128 points in chunks of the scratch's capacity (rbg_asm.cuh
+    kChunkSteps): dense sub-tiles forced through rbg_set_tile_divisor, every chunk, panel
+    shape and flush path against the oracle."""
+    refs = configs.halton(1, m, dim)
+    alpha = configs._alpha_for(m, per_support, dim)
+    rng = np.random.default_rng(100 + dim + family)
+    pts = rng.random((n, dim))
+    h = rng.standard_normal(n)
+    with api.Engine(0) as e:
+        e.set_centres(refs, api.KernelSpec(family, alpha))
+        e.set_tile_divisor(divisor)
+        e.assemble(pts, h)
+        lay = e.layout_info()
+        per_sub = n * lay["sub_edge"] ** dim  # uniform points in the unit cube
+        assert lay["max_sub_centres"] > 56 and per_sub > 128 and lay["n_fallback"] == 0, lay
+        rp, cols = e.pattern()
+        s = e.system()
+    orp, ocols = po.pattern(refs, alpha)
+    assert np.array_equal(rp, orp) and np.array_equal(cols, ocols)
+    ov, orhs, ohits = po.assemble(pts, h, refs, family, alpha, orp, ocols)
+    assert np.array_equal(s["hits"].astype(np.uint64), ohits)
+    assert scaled(s["values"], ov) < TOL_SYS and max(entrywise(s["values"], ov, orp, ocols)) < TOL_SYS
+    assert scaled(s["rhs"], orhs) < TOL_SYS
+
+
 def test_slab_accumulation_equals_single(eng):
     xy, h = configs.points("cfg2", n=50_000)
     refs = configs.centres("cfg2")
