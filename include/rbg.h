@@ -205,12 +205,19 @@ rbg_status rbg_support_counts(rbg_ctx* ctx, const double* points, uint64_t nq, u
                               uint64_t* sum_k2);
 /* fp64 FMA throughput of this GPU (TFLOP/s, FMA = 2 flops), microbenchmark. */
 rbg_status rbg_fp64_peak(rbg_ctx* ctx, double* tflops);
-/* The assembly kernel's phi against the reference arithmetic (kernel.hpp:42-62
+/* The reference-exact phi of the numeric kernels (border, and the assembly's
+ * inclusion test) against the reference arithmetic (kernel.hpp:42-62
  * with sqrt_rn, kdtree.cpp:64,74) on n sampled distances of every magnitude:
  * mismatches = inclusion differences + (wendland-3-0/3-1) values not bitwise
  * equal (must be 0); max relative / absolute error of phi. */
 rbg_status rbg_phi_selftest(rbg_ctx* ctx, int kernel_family, double alpha, uint64_t n, uint64_t seed,
                             uint64_t* mismatches, double* max_rel, double* max_abs);
+/* The same sampling for the variant the assembly's k-loop evaluates (one
+ * Goldschmidt step + residual correction, FMA-contracted polynomial; A is
+ * never output): mismatches = inclusion differences only (must be 0); max
+ * relative error over values >= 1e-6; max absolute error. */
+rbg_status rbg_phi_selftest_fast(rbg_ctx* ctx, int kernel_family, double alpha, uint64_t n, uint64_t seed,
+                                 uint64_t* mismatches, double* max_rel, double* max_abs);
 /* Assembly layout knobs (performance only; results are unaffected beyond
  * fp64 summation order): sub-tile edge = support radius / divisor (1..16,
  * 0 = automatic from the point density) and super-tile = S x S (x S)

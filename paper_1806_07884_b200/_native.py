@@ -112,6 +112,8 @@ _SIGS = {
     "rbg_assembly_times": (C.c_int, [_P, _D, _D]),
     "rbg_phi_selftest": (C.c_int, [_P, C.c_int, C.c_double, _U64, _U64, C.POINTER(_U64),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "rbg_phi_selftest_fast": (C.c_int, [_P, C.c_int, C.c_double, _U64, _U64, C.POINTER(_U64),
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "rbg_set_tile_divisor": (C.c_int, [_P, C.c_double]),
     "rbg_set_super_factor": (C.c_int, [_P, C.c_int]),
     "rbg_get_layout_info": (C.c_int, [_P, C.POINTER(LayoutInfo)]),

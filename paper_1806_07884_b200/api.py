@@ -115,11 +115,12 @@ class Engine:
         self._check(self._L.rbg_get_layout_info(self._ctx, C.byref(info)))
         return {k: getattr(info, k) for k, _ in info._fields_}
 
-    def phi_selftest(self, family: int, alpha: float, n: int = 1 << 24, seed: int = 1) -> dict:
-        """The assembly kernel's phi against the reference arithmetic (rbg_phi_selftest)."""
+    def phi_selftest(self, family: int, alpha: float, n: int = 1 << 24, seed: int = 1, fast: bool = False) -> dict:
+        """The numeric kernels' phi against the reference arithmetic (rbg_phi_selftest; fast = the
+        variant of the assembly's k-loop, rbg_phi_selftest_fast)."""
         bad, rel, ab = C.c_uint64(), C.c_double(), C.c_double()
-        self._check(self._L.rbg_phi_selftest(self._ctx, int(family), float(alpha), n, seed, C.byref(bad),
-                                             C.byref(rel), C.byref(ab)))
+        fn = self._L.rbg_phi_selftest_fast if fast else self._L.rbg_phi_selftest
+        self._check(fn(self._ctx, int(family), float(alpha), n, seed, C.byref(bad), C.byref(rel), C.byref(ab)))
         return {"mismatches": int(bad.value), "max_rel": rel.value, "max_abs": ab.value}
 
     def set_stream(self, stream: int | None) -> None:

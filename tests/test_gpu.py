@@ -334,6 +334,17 @@ def test_assembly_phi_inclusion_exact_and_value_close(eng, family):
             assert r["max_rel"] < 4e-15, (alpha, r)
 
 
+@pytest.mark.parametrize("family", [0, 1, 2, 3])
+def test_assembly_fast_phi_inclusion_exact_and_value_within_ulps(eng, family):
+    """phi_k3<FAM, true> (what the assembly's k-loop evaluates): the same bit-exact
+    inclusion; values within a few ulp of the reference's away from the support's edge and
+    within 4e-15 absolutely everywhere (phi <= 3: a few ulp; measured 2.7e-15, relative 1.3e-14)."""
+    for alpha in (0.25, 1.0, 10.2333, 280.2496, 1e6):
+        r = eng.phi_selftest(family, alpha, 1 << 24, 54321, fast=True)
+        assert r["mismatches"] == 0, (alpha, r)
+        assert r["max_abs"] < 4e-15 and r["max_rel"] < 1e-12, (alpha, r)
+
+
 @pytest.mark.parametrize("div,sup", [(2.0, 1), (3.0, 2), (5.0, 3), (6.0, 4), (8.0, 2), (12.0, 5)])
 def test_layout_does_not_change_results(eng, div, sup):
     # sub-tile divisor / super-tile factor are performance knobs only
