@@ -174,7 +174,9 @@ int env_int(const char* name, int dflt) {
 // about 32 points (edge r/2 .. r/4) assembled in direct mode (one sub-tile per super-tile, register
 // tiles reduced straight into the CSR values: a 3-D super-tile accumulator
 // would not fit shared memory).
-static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* span, int& q, int& S) {
+constexpr uint64_t kFineAfter = 2;  // assemblies on a centre set before its 3-D tiling is refined
+
+static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* span, int& q, int& S, bool& fine) {
     const int dim = ctx->dim;
     const double r = ctx->radius;
     double vol = 1.0;
@@ -184,9 +186,15 @@ static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* s
         const double e = std::sqrt(34.0 / rho);
         q = std::max(2, std::min(16, (int)std::lround(r / e)));
         S = q >= 9 ? 4 : q >= 7 ? 3 : 2;
-    } else {  // about 32 points per cube (cfg3: r/3, 28 points: K3 5.4 ms; r/2 7.9 ms; r/4 10.6 ms)
+    } else {  // about 32 points per cube (cfg3: r/3, 28 points: K3 5.4 ms; r/2 7.9 ms; r/4 10.6 ms) --
+        // once the centre set is reused: the finer tiling's slot maps cost more to build than one
+        // assembly gains (cfg3: layout 6.7 -> 10.5 ms for 2.4 ms of K3), so the first assembly of
+        // a centre set runs on r/2 cubes and ensure_layout upgrades once it has been used
+        // kFineAfter times (rent-or-buy: the regret of either choice stays within ~2x)
         const double e = std::cbrt(32.0 / rho);
-        q = std::max(2, std::min(4, (int)std::lround(r / e)));
+        const int qf = std::max(2, std::min(4, (int)std::lround(r / e)));
+        q = fine ? qf : 2;
+        fine = q == qf;  // (nothing to upgrade to when the density asks for r/2 anyway)
         S = 1;
     }
     // small problems: shrink the super-tiles until there are at least two per
@@ -206,6 +214,7 @@ static void choose_layout(const rbg_ctx* ctx, uint64_t n_points, const double* s
     const int qe = env_int("RBG_SUB_DIV", 0), se = env_int("RBG_SUPER", 0);
     if (qe > 0) q = qe;
     if (se > 0) S = se;
+    if (ctx->sub_div_req > 0 || ctx->super_req > 0 || qe > 0 || se > 0) fine = true;  // explicit choices are final
 }
 
 void build_layout(rbg_ctx* ctx, uint64_t n_points) {
@@ -219,7 +228,8 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     double span[3] = {1, 1, 1};
     for (int d = 0; d < dim; ++d) span[d] = (double)ctx->grid.n[d] * ctx->grid.edge;
     int q = 4, S = 2;
-    choose_layout(ctx, n_points, span, q, S);
+    bool fine = dim == 2 || L.uses >= kFineAfter;
+    choose_layout(ctx, n_points, span, q, S, fine);
     double e = r / q;
     int64_t nsup[3] = {1, 1, 1};
     uint64_t n_super = 1;
@@ -416,6 +426,7 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
     ctx->tile_pptr.reserve(L.n_keys + 1);
     RBG_CUDA(cudaStreamSynchronize(st));
     L.built = true;
+    L.fine = fine;
     L.n_built = n_points;
     L.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -426,7 +437,8 @@ void build_layout(rbg_ctx* ctx, uint64_t n_points) {
 void ensure_layout(rbg_ctx* ctx, uint64_t n_points) {
     const AsmLayout& L = ctx->lay;
     const bool pinned_choice = ctx->sub_div_req > 0 || ctx->super_req > 0;
-    if (L.built && (pinned_choice || (n_points <= 4 * L.n_built && L.n_built <= 4 * n_points))) return;
+    const bool upgrade = L.built && !pinned_choice && !L.fine && L.uses >= kFineAfter;  // 3-D, third assembly
+    if (L.built && !upgrade && (pinned_choice || (n_points <= 4 * L.n_built && L.n_built <= 4 * n_points))) return;
     build_layout(ctx, n_points);
 }
 

@@ -122,11 +122,22 @@ def test_cfg3_full_size(eng):
     cfg = configs.CONFIGS["cfg3"]
     xyz, h = configs.points("cfg3")
     refs = configs.centres("cfg3")
-    rp, cols, ov, orhs, _ = check_system(eng, xyz, h, refs, 3, cfg.alpha)
+    rp, cols, ov, orhs, ohits = check_system(eng, xyz, h, refs, 3, cfg.alpha)
+    assert eng.layout_info()["sub_div"] == 2  # first assembly of a centre set: r/2 cubes
     c, diag = eng.solve()
     res = np.linalg.norm(sym_matvec(rp, cols, ov, c) - orhs) / np.linalg.norm(orhs)
     assert res < 1e-9, res
     check_eval_and_report(eng, refs, c, 3, cfg.alpha, xyz[:200_000], h[:200_000])
+    # from the third assembly on the same centres the tiling is the density-derived one (r/3
+    # here: staged slot maps, two-panel sub-tiles); same system against the same oracle values
+    eng.assemble(xyz, h)
+    assert eng.layout_info()["sub_div"] == 2
+    eng.assemble(xyz, h)
+    assert eng.layout_info()["sub_div"] == 3
+    s = eng.system()
+    assert np.array_equal(s["hits"].astype(np.uint64), ohits)
+    assert scaled(s["values"], ov) < TOL_SYS and max(entrywise(s["values"], ov, rp, cols)) < TOL_SYS
+    assert scaled(s["rhs"], orhs) < TOL_SYS
 
 
 def test_cfg4_four_million_points(eng):
