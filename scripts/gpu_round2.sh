@@ -19,9 +19,9 @@ timeout 2400 ncu --set full --clock-control none -c 120 -o /tmp/${TAG}_all pytho
 ncu -i /tmp/${TAG}_all.ncu-rep --page raw --csv > gpurun_out/${TAG}_all_raw.csv 2>/dev/null
 python scripts/ncu_table.py gpurun_out/${TAG}_all_raw.csv > gpurun_out/${TAG}_all_table.md 2>&1
 rm -f /tmp/${TAG}_all.ncu-rep
-CMD2="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+CMD2="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"  # (3-D: the tiling is refined at the third assembly)
 cap() {  # cap NAME KERNEL_REGEX CONFIG
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 -o /tmp/${TAG}_$1 $CMD2 --config $3 > gpurun_out/${TAG}_ncu_$1.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$2 -s 3 -c 1 -o /tmp/${TAG}_$1 $CMD2 --config $3 > gpurun_out/${TAG}_ncu_$1.log 2>&1
   ncu -i /tmp/${TAG}_$1.ncu-rep --page raw --csv > gpurun_out/${TAG}_$1_raw.csv 2>/dev/null
   python scripts/ncu_raw_summary.py gpurun_out/${TAG}_$1_raw.csv > gpurun_out/${TAG}_$1_summary.txt 2>&1
   ncu -i /tmp/${TAG}_$1.ncu-rep --page source --csv --print-source sass,cuda > /tmp/${TAG}_$1_src.csv 2>/dev/null
